@@ -1,0 +1,114 @@
+/*
+ * fgmatte_b200 -- C ABI of the B200 (sm_100a) multi-level foreground /
+ * background estimator (arXiv 2006.14970).
+ *
+ * Every entry point replaces one reference interface (paths relative to
+ * /root/reference/proj):
+ *
+ *   fgm_params               <- fgmatte::MlParams            include/fgmatte/multilevel.hpp:12-20
+ *   fgm_params_validate      <- MlParams::validate           src/multilevel.cpp:10-15
+ *   fgm_level_schedule       <- fgmatte::level_schedule      src/multilevel.cpp:17-44
+ *   fgm_ml_solve_f32         <- fgmatte::ml_foreground_background  src/multilevel.cpp:141-166
+ *   fgm_ml_solve_host_f32/64 <- the same, host buffers (the reference's own
+ *                               call shape: planar Image in, planar Image out,
+ *                               include/fgmatte/image.hpp:12-26)
+ *   fgm_ml_solve_levels_f32  <- the same, plus every level's F/B (debug hook
+ *                               for per-level parity; the reference keeps them
+ *                               internal, multilevel.cpp:157-164)
+ *   fgm_batch_solve_f32      <- N independent ml_foreground_background calls
+ *                               (the reference is reentrant)
+ *   fgm_resize_f32           <- fgmatte::resize              src/image.cpp:114-133
+ *   fgm_sweep_passes_f32     <- `iterations` x sweep         src/multilevel.cpp:81-121, 162-163
+ *
+ * Conventions: planar fp32 (plane(c)[y*w + x], as image.hpp:22-26), image = 3
+ * planes, alpha = 1 plane, fg/bg = 3 planes each.  "Device" entry points take
+ * device pointers and enqueue on `stream` (a cudaStream_t, NULL = legacy
+ * default stream) without synchronising; "host" entry points take host
+ * pointers and return when the result is in host memory.
+ *
+ * Status codes: FGM_OK (0); FGM_INVALID_ARGUMENT (1) where the reference
+ * throws std::invalid_argument (same message text, fgm_last_error());
+ * FGM_RUNTIME_ERROR (2) for CUDA / runtime failures.  There is no CPU
+ * fallback: without a usable sm_100 device every solve returns 2.
+ * fgm_last_error() is thread-local.  All entry points are reentrant.
+ */
+#ifndef FGMATTE_B200_H
+#define FGMATTE_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FGM_OK 0
+#define FGM_INVALID_ARGUMENT 1
+#define FGM_RUNTIME_ERROR 2
+
+/* MlParams (multilevel.hpp:12-20), named as in BASELINE.json's north_star. */
+typedef struct fgm_params {
+    double regularization;  /* eps_r  (> 0)               multilevel.hpp:14 */
+    double gradient_weight; /* omega  (>= 0)              multilevel.hpp:13 */
+    int n_small_iterations; /* iters_low  (>= 1)          multilevel.hpp:16 */
+    int n_big_iterations;   /* iters_high (>= 1)          multilevel.hpp:17 */
+    int small_size;         /* low_res_threshold (>= 1)   multilevel.hpp:15 */
+} fgm_params;
+
+/* Reference defaults (multilevel.hpp:13-17): eps_r 5e-3, omega 0.1, 10, 2, 32. */
+void fgm_params_default(fgm_params* p);
+
+int fgm_params_validate(const fgm_params* p);
+
+/* Writes up to `cap` levels (coarse -> full); returns the level count, or
+ * -FGM_INVALID_ARGUMENT. */
+int fgm_level_schedule(int w, int h, const fgm_params* p, int* out_w, int* out_h, int* out_iters, int cap);
+
+/* Device pointers, asynchronous on `stream`. */
+int fgm_ml_solve_f32(const float* image, const float* alpha, int w, int h, const fgm_params* p, float* fg, float* bg,
+                     void* stream);
+
+/* Host pointers (pageable or pinned); synchronous. */
+int fgm_ml_solve_host_f32(const float* image, const float* alpha, int w, int h, const fgm_params* p, float* fg,
+                          float* bg);
+/* fp64 host planes, as the reference's Image/AlphaMatte hold them; converted to
+ * fp32 on the device (K5), results converted back.  Used by the C++ drop-in. */
+int fgm_ml_solve_host_f64(const double* image, const double* alpha, int w, int h, const fgm_params* p, double* fg,
+                          double* bg);
+
+/* Device pointers.  level_fg[l] / level_bg[l] (3 planes of level l's size, or
+ * NULL) receive each level's F/B after its sweeps. */
+int fgm_ml_solve_levels_f32(const float* image, const float* alpha, int w, int h, const fgm_params* p, float* fg,
+                            float* bg, float* const* level_fg, float* const* level_bg, int n_levels, void* stream);
+
+/* A batch of independent images, device pointers, one stream, batched
+ * level-by-level launches. */
+int fgm_batch_solve_f32(int n_images, const float* const* images, const float* const* alphas, const int* widths,
+                        const int* heights, const fgm_params* p, float* const* fgs, float* const* bgs, void* stream);
+
+/* Bilinear, centre-aligned, edge-clamped resize of `nplanes` planes with
+ * clamp01, identity copy at equal size (image.cpp:71-133).  Device pointers. */
+int fgm_resize_f32(const float* src, int sw, int sh, int nplanes, float* dst, int dw, int dh, void* stream);
+
+/* `iterations` exact Gauss-Seidel scanline sweeps of one level, given the
+ * level's image/alpha and initial F/B (device pointers; fg_out/bg_out may not
+ * alias the inputs).  The GPU counterpart of multilevel.cpp:162-163. */
+int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg_in, const float* bg_in, int w,
+                         int h, int iterations, double regularization, double gradient_weight, float* fg_out,
+                         float* bg_out, void* stream);
+
+/* Profiling: when enabled, every kernel launch of the solver is bracketed by
+ * CUDA events on its stream; fgm_kernel_stats() synchronises on the recorded
+ * events and reports, for kernel class `which` (0 = big-level sweep K3,
+ * 1 = resample K1/K2, 2 = coarse levels K4), the launch count, the summed
+ * device milliseconds and the algorithmic HBM bytes of those launches
+ * ("Roofline").  fgm_profile_reset() clears the counters. */
+void fgm_profile_enable(int on);
+void fgm_profile_reset(void);
+int fgm_kernel_stats(int which, long long* launches, double* ms, double* alg_bytes);
+
+const char* fgm_last_error(void);
+int fgm_device_count(void);
+const char* fgm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FGMATTE_B200_H */

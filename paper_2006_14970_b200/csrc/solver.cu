@@ -1,0 +1,726 @@
+// Host orchestration and the extern "C" boundary (include/fgmatte_b200.h).
+//
+// A solve is planned on the host (level schedule, coarse/big split, pass
+// decomposition, workspace carving -- all O(levels)) and then enqueued on one
+// stream: one K4 launch for every image's coarse levels, then, level by level
+// from the coarse end, one batched K1/K2 launch and one K3 launch per pass.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <bit>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fgmatte_b200.h"
+#include "fgm_internal.h"
+
+namespace fgm {
+namespace {
+
+thread_local std::string g_err;
+
+struct InvalidArgument : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct RuntimeError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw RuntimeError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct Level {
+    int w, h, iters;
+};
+
+// MlParams::validate (multilevel.cpp:10-15), same messages.
+void validate(const fgm_params* p) {
+    if (!p) throw InvalidArgument("fgm_params: null");
+    if (!(p->gradient_weight >= 0.0)) throw InvalidArgument("MlParams: omega must be >= 0");
+    if (!(p->regularization > 0.0)) throw InvalidArgument("MlParams: eps_r must be > 0");
+    if (p->n_small_iterations < 1 || p->n_big_iterations < 1)
+        throw InvalidArgument("MlParams: iteration counts must be >= 1");
+    if (p->small_size < 1) throw InvalidArgument("MlParams: low_res_threshold must be >= 1");
+    // fp32 representability of the two weights (the only fp32 restriction).
+    const float e = float(p->regularization), o = float(p->gradient_weight);
+    if (!(e >= 1.17549435e-38f) || !std::isfinite(e) || !std::isfinite(o))
+        throw InvalidArgument("MlParams: eps_r / omega not representable in fp32");
+}
+
+// level_schedule (multilevel.cpp:17-44): same integer/libm arithmetic.
+std::vector<Level> schedule(int W, int H, const fgm_params* p) {
+    if (W < 1 || H < 1) throw InvalidArgument("level_schedule: size must be >= 1x1");
+    validate(p);
+    const unsigned m = unsigned(std::max(W, H));
+    int n = m > 1 ? int(std::bit_width(m - 1)) : 0;
+    if (n < 1) n = 1;
+    std::vector<Level> out;
+    out.reserve(size_t(n));
+    for (int l = 1; l <= n; ++l) {
+        int w, h;
+        if (l == n) {
+            w = W;
+            h = H;
+        } else {
+            const double e = double(l) / double(n);
+            w = int(std::llround(std::pow(double(W), e)));
+            h = int(std::llround(std::pow(double(H), e)));
+        }
+        const int it = std::max(w, h) <= p->small_size ? p->n_small_iterations : p->n_big_iterations;
+        out.push_back({w, h, it});
+    }
+    return out;
+}
+
+// Split `iters` sweeps into fused passes with a compiled K.
+std::vector<int> passes_for(int iters) {
+    static const int ks[] = {8, 4, 3, 2, 1};
+    std::vector<int> out;
+    while (iters > 0) {
+        for (int k : ks)
+            if (k <= iters) {
+                out.push_back(k);
+                iters -= k;
+                break;
+            }
+    }
+    return out;
+}
+
+// ---- profiling -------------------------------------------------------------
+struct ProfRec {
+    cudaEvent_t a, b;
+    int which;
+    double bytes;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+long long g_launches[3] = {0, 0, 0};
+double g_ms[3] = {0, 0, 0}, g_bytes[3] = {0, 0, 0};
+
+struct ProfScope {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t s;
+    int which;
+    double bytes;
+    ProfScope(cudaStream_t s_, int which_, double bytes_) : s(s_), which(which_), bytes(bytes_) {
+        bool on;
+        {
+            std::lock_guard<std::mutex> g(g_prof_mu);
+            on = g_prof_on;
+        }
+        if (on) {
+            ck(cudaEventCreate(&a), "cudaEventCreate");
+            ck(cudaEventCreate(&b), "cudaEventCreate");
+            ck(cudaEventRecord(a, s), "cudaEventRecord");
+        }
+    }
+    ~ProfScope() {
+        if (!a) return;
+        cudaEventRecord(b, s);
+        std::lock_guard<std::mutex> g(g_prof_mu);
+        g_prof.push_back({a, b, which, bytes});
+    }
+};
+
+void prof_drain() {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (auto& r : g_prof) {
+        cudaEventSynchronize(r.b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        g_launches[r.which] += 1;
+        g_ms[r.which] += ms;
+        g_bytes[r.which] += r.bytes;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+}
+
+// ---- device checks ---------------------------------------------------------
+void require_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw RuntimeError(std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                           "); fgmatte_b200 has no CPU fallback");
+    static bool pool_set = false;
+    if (!pool_set) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_set = true;
+    }
+}
+
+// ---- stream-ordered workspace ----------------------------------------------
+struct Arena {
+    char* base = nullptr;
+    size_t size = 0, off = 0;
+    cudaStream_t s = nullptr;
+    void reserve(size_t bytes, cudaStream_t st) {
+        s = st;
+        size = bytes;
+        if (bytes) ck(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, s), "cudaMallocAsync");
+    }
+    template <class T>
+    T* take(size_t count) {
+        const size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+        if (off + bytes > size) throw RuntimeError("internal: arena overflow");
+        T* p = reinterpret_cast<T*>(base + off);
+        off += bytes;
+        return p;
+    }
+    ~Arena() {
+        if (base) cudaFreeAsync(base, s);
+    }
+};
+
+inline size_t al(size_t bytes) { return (bytes + 255) & ~size_t(255); }
+
+// ---- the batched multi-level solve ----------------------------------------
+struct ImageIO {
+    const float* img;
+    const float* alpha;
+    int W, H;
+    float* fg;
+    float* bg;
+    float* const* level_fg;  // optional per-level dumps (n levels)
+    float* const* level_bg;
+};
+
+struct Plan {
+    ImageIO io;
+    std::vector<Level> lv;
+    int nc = 0;                      // number of coarse levels (K4)
+    size_t max_sub = 0;              // max pixels over levels < n-1
+    size_t max_lvl = 0;              // max pixels over all levels
+    bool multipass = false;
+    size_t stream_floats = 0;        // per pass, max over big levels
+    int max_bands = 0;
+    // carved workspace
+    float *lvlIA = nullptr, *fbInit = nullptr, *fbTmp = nullptr, *fbOut = nullptr, *stream = nullptr;
+};
+
+void plan_image(Plan& P, const fgm_params* p) {
+    P.lv = schedule(P.io.W, P.io.H, p);
+    const int n = int(P.lv.size());
+    P.nc = 0;
+    while (P.nc < n && P.nc < kMaxCoarseLevels && size_t(P.lv[size_t(P.nc)].w) * P.lv[size_t(P.nc)].h <= size_t(kCoarseCap))
+        ++P.nc;
+    if (P.nc == 0) throw RuntimeError("internal: first level exceeds the coarse capacity");
+    for (int l = 0; l < n; ++l) {
+        const size_t px = size_t(P.lv[size_t(l)].w) * P.lv[size_t(l)].h;
+        P.max_lvl = std::max(P.max_lvl, px);
+        if (l < n - 1) P.max_sub = std::max(P.max_sub, px);
+        if (l >= P.nc) {
+            for (int K : passes_for(P.lv[size_t(l)].iters)) {
+                P.stream_floats = std::max(P.stream_floats, sweep_stream_floats(P.lv[size_t(l)].w, P.lv[size_t(l)].h, K));
+                P.max_bands = std::max(P.max_bands, sweep_bands(P.lv[size_t(l)].h, K));
+            }
+            if (passes_for(P.lv[size_t(l)].iters).size() > 1) P.multipass = true;
+        }
+    }
+}
+
+size_t plan_bytes(const Plan& P) {
+    if (P.nc == int(P.lv.size())) return 0;
+    size_t b = 0;
+    b += al(4 * P.max_sub * sizeof(float));                       // lvlIA
+    b += al(6 * P.max_lvl * sizeof(float));                       // fbInit
+    if (P.multipass) b += al(6 * P.max_lvl * sizeof(float));      // fbTmp
+    b += al(6 * std::max<size_t>(P.max_sub, 1) * sizeof(float));  // fbOut
+    b += al(P.stream_floats * sizeof(float));
+    return b;
+}
+
+void carve(Plan& P, Arena& A) {
+    if (P.nc == int(P.lv.size())) return;
+    P.lvlIA = A.take<float>(4 * P.max_sub);
+    P.fbInit = A.take<float>(6 * P.max_lvl);
+    if (P.multipass) P.fbTmp = A.take<float>(6 * P.max_lvl);
+    P.fbOut = A.take<float>(6 * std::max<size_t>(P.max_sub, 1));
+    P.stream = A.take<float>(P.stream_floats);
+}
+
+// Host-side staging of every job descriptor of one solve: one H2D copy and
+// one memset of the dependency counters per solve.
+struct JobStage {
+    std::vector<unsigned char> host;
+    std::vector<size_t> sweep_offsets;  // SweepJob records whose `progress` holds a counter index
+    size_t counters = 0;
+    template <class T>
+    size_t push(const std::vector<T>& v) {
+        const size_t off = al(host.size());
+        host.resize(off + v.size() * sizeof(T));
+        std::memcpy(host.data() + off, v.data(), v.size() * sizeof(T));
+        return off;
+    }
+};
+
+enum LaunchKind { kCoarse, kResample, kSweep, kCopy };
+struct LaunchRec {
+    LaunchKind kind;
+    int K, njobs, total_bands;
+    size_t job_off, ticket;
+    long long max_rows;
+    double bytes;
+    void* dst = nullptr;
+    const void* src = nullptr;
+};
+
+void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s) {
+    validate(p);
+    require_device();
+    const float eps = float(p->regularization), omega = float(p->gradient_weight);
+    std::vector<Plan> plans(ios.size());
+    for (size_t i = 0; i < ios.size(); ++i) {
+        if (!ios[i].img || !ios[i].alpha || !ios[i].fg || !ios[i].bg) throw InvalidArgument("null buffer");
+        plans[i].io = ios[i];
+        plan_image(plans[i], p);
+    }
+    size_t ws = 0;
+    int J = 0;
+    for (auto& P : plans) {
+        ws += plan_bytes(P);
+        J = std::max(J, int(P.lv.size()) - P.nc);
+    }
+    Arena W;
+    W.reserve(ws, s);
+    for (auto& P : plans) carve(P, W);
+
+    JobStage st;
+    std::vector<LaunchRec> launches;
+
+    // ---- K4: every image's coarse prefix ---------------------------------
+    {
+        std::vector<CoarseJob> cj(plans.size());
+        double bytes = 0;
+        for (size_t i = 0; i < plans.size(); ++i) {
+            const Plan& P = plans[i];
+            CoarseJob& c = cj[i];
+            std::memset(&c, 0, sizeof(c));
+            c.img = P.io.img;
+            c.alpha = P.io.alpha;
+            c.W = P.io.W;
+            c.H = P.io.H;
+            c.nlev = P.nc;
+            for (int l = 0; l < P.nc; ++l) {
+                c.lw[l] = P.lv[size_t(l)].w;
+                c.lh[l] = P.lv[size_t(l)].h;
+                c.lit[l] = P.lv[size_t(l)].iters;
+                if (P.io.level_fg) {
+                    c.lvl_fg[l] = P.io.level_fg[l];
+                    c.lvl_bg[l] = P.io.level_bg[l];
+                }
+            }
+            const size_t n = size_t(P.lv[size_t(P.nc - 1)].w) * P.lv[size_t(P.nc - 1)].h;
+            if (P.nc == int(P.lv.size())) {
+                c.fg_out = P.io.fg;
+                c.bg_out = P.io.bg;
+            } else {
+                c.fg_out = P.fbOut;
+                c.bg_out = P.fbOut + 3 * n;
+            }
+            bytes += 24.0 * double(n);
+        }
+        launches.push_back({kCoarse, 0, int(cj.size()), 0, st.push(cj), 0, 0, bytes});
+    }
+
+    // ---- big levels, aligned so that every image's top level is step J-1 --
+    for (int j = 0; j < J; ++j) {
+        std::vector<ResampleJob> rj;
+        long long max_rows = 0;
+        double rbytes = 0;
+        struct Active {
+            Plan* P;
+            int l;
+        };
+        std::vector<Active> act;
+        for (auto& P : plans) {
+            const int n = int(P.lv.size());
+            const int l = n - J + j;
+            if (l < P.nc) continue;
+            act.push_back({&P, l});
+            const Level L = P.lv[size_t(l)], Lp = P.lv[size_t(l - 1)];
+            const long long px = (long long)L.w * L.h, ppx = (long long)Lp.w * Lp.h;
+            const long long fpx = (long long)P.io.W * P.io.H;
+            if (l < n - 1) {
+                rj.push_back({P.io.img, P.lvlIA, P.io.W, P.io.H, L.w, L.h, 3, fpx, px});
+                rj.push_back({P.io.alpha, P.lvlIA + 3 * px, P.io.W, P.io.H, L.w, L.h, 1, fpx, px});
+                rbytes += 4.0 * 4 * (double(px) + std::min<double>(double(fpx), 4.0 * px));
+            }
+            rj.push_back({P.fbOut, P.fbInit, Lp.w, Lp.h, L.w, L.h, 6, ppx, px});
+            rbytes += 4.0 * 6 * (double(px) + double(ppx));
+            max_rows = std::max<long long>(max_rows, L.h);
+        }
+        if (act.empty()) continue;
+        launches.push_back({kResample, 0, int(rj.size()), 0, st.push(rj), 0, max_rows, rbytes});
+        size_t max_passes = 0;
+        for (auto& a : act) max_passes = std::max(max_passes, passes_for(a.P->lv[size_t(a.l)].iters).size());
+        for (size_t pi = 0; pi < max_passes; ++pi) {
+            for (int K : {8, 4, 3, 2, 1}) {
+                std::vector<SweepJob> sj;
+                int total = 0;
+                double sbytes = 0;
+                const size_t ticket = st.counters++;
+                for (auto& a : act) {
+                    Plan& P = *a.P;
+                    const std::vector<int> ps = passes_for(P.lv[size_t(a.l)].iters);
+                    if (pi >= ps.size() || ps[pi] != K) continue;
+                    const Level L = P.lv[size_t(a.l)];
+                    const int n = int(P.lv.size());
+                    const long long px = (long long)L.w * L.h;
+                    const bool last = pi + 1 == ps.size();
+                    const bool top = a.l == n - 1;
+                    float* bufs[2] = {P.fbTmp, P.fbInit};  // pass ping-pong
+                    const float* in = pi == 0 ? P.fbInit : bufs[(pi - 1) & 1];
+                    SweepJob J1{};
+                    J1.img = top ? P.io.img : P.lvlIA;
+                    J1.alpha = top ? P.io.alpha : P.lvlIA + 3 * px;
+                    J1.fg_in = in;
+                    J1.bg_in = in + 3 * px;
+                    if (last) {
+                        J1.fg_out = top ? P.io.fg : P.fbOut;
+                        J1.bg_out = top ? P.io.bg : P.fbOut + 3 * px;
+                    } else {
+                        J1.fg_out = bufs[pi & 1];
+                        J1.bg_out = bufs[pi & 1] + 3 * px;
+                    }
+                    J1.stream = P.stream;
+                    J1.pstride = px;
+                    J1.w = L.w;
+                    J1.h = L.h;
+                    J1.nb = sweep_bands(L.h, K);
+                    J1.band_base = total;
+                    J1.progress = reinterpret_cast<unsigned*>(uintptr_t(st.counters));  // patched below
+                    st.counters += size_t(J1.nb);
+                    total += J1.nb;
+                    sbytes += 64.0 * double(px);
+                    sj.push_back(J1);
+                }
+                if (sj.empty()) {
+                    --st.counters;
+                    continue;
+                }
+                const size_t off = st.push(sj);
+                for (size_t k = 0; k < sj.size(); ++k) st.sweep_offsets.push_back(off + k * sizeof(SweepJob));
+                launches.push_back({kSweep, K, int(sj.size()), total, off, ticket, 0, sbytes});
+            }
+        }
+        for (auto& a : act) {  // per-level dumps (debug API)
+            Plan& P = *a.P;
+            if (!P.io.level_fg) continue;
+            const Level L = P.lv[size_t(a.l)];
+            const size_t px = size_t(L.w) * L.h;
+            const bool top = a.l == int(P.lv.size()) - 1;
+            const float* f = top ? P.io.fg : P.fbOut;
+            const float* b = top ? P.io.bg : P.fbOut + 3 * px;
+            if (P.io.level_fg[a.l])
+                launches.push_back({kCopy, 0, 0, 0, 0, 0, 0, double(3 * px * sizeof(float)), P.io.level_fg[a.l], f});
+            if (P.io.level_bg[a.l])
+                launches.push_back({kCopy, 0, 0, 0, 0, 0, 0, double(3 * px * sizeof(float)), P.io.level_bg[a.l], b});
+        }
+    }
+
+    Arena B;
+    B.reserve(al(st.host.size()) + al(std::max<size_t>(st.counters, 1) * sizeof(unsigned)), s);
+    unsigned char* djobs = B.take<unsigned char>(st.host.size());
+    unsigned* dctr = B.take<unsigned>(std::max<size_t>(st.counters, 1));
+    for (size_t off : st.sweep_offsets) {
+        SweepJob* sjp = reinterpret_cast<SweepJob*>(st.host.data() + off);
+        sjp->progress = dctr + reinterpret_cast<uintptr_t>(sjp->progress);
+    }
+    ck(cudaMemsetAsync(dctr, 0, std::max<size_t>(st.counters, 1) * sizeof(unsigned), s), "cudaMemsetAsync");
+    ck(cudaMemcpyAsync(djobs, st.host.data(), st.host.size(), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
+
+    for (const LaunchRec& r : launches) {
+        switch (r.kind) {
+            case kCoarse: {
+                ProfScope ps(s, 2, r.bytes);
+                ck(launch_coarse(reinterpret_cast<const CoarseJob*>(djobs + r.job_off), r.njobs, eps, omega, s),
+                   "coarse_kernel");
+                break;
+            }
+            case kResample: {
+                ProfScope ps(s, 1, r.bytes);
+                ck(launch_resample(reinterpret_cast<const ResampleJob*>(djobs + r.job_off), r.njobs, r.max_rows, s),
+                   "resample_kernel");
+                break;
+            }
+            case kSweep: {
+                ProfScope ps(s, 0, r.bytes);
+                ck(launch_sweep(r.K, reinterpret_cast<const SweepJob*>(djobs + r.job_off), r.njobs, r.total_bands,
+                                dctr + r.ticket, eps, omega, s),
+                   "sweep_kernel");
+                break;
+            }
+            case kCopy:
+                ck(cudaMemcpyAsync(r.dst, r.src, size_t(r.bytes), cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync");
+                break;
+        }
+    }
+}
+
+template <class F>
+int guarded(F&& fn) {
+    try {
+        fn();
+        return FGM_OK;
+    } catch (const InvalidArgument& e) {
+        g_err = e.what();
+        return FGM_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FGM_RUNTIME_ERROR;
+    }
+}
+
+void check_dims(int w, int h) {
+    if (w < 1 || h < 1)
+        throw InvalidArgument("Image: dimensions must be >= 1, got " + std::to_string(w) + "x" + std::to_string(h));
+}
+
+}  // namespace
+}  // namespace fgm
+
+using namespace fgm;
+
+extern "C" {
+
+void fgm_params_default(fgm_params* p) {
+    if (!p) return;
+    p->regularization = 5e-3;
+    p->gradient_weight = 0.1;
+    p->n_small_iterations = 10;
+    p->n_big_iterations = 2;
+    p->small_size = 32;
+}
+
+int fgm_params_validate(const fgm_params* p) {
+    return guarded([&] { validate(p); });
+}
+
+int fgm_level_schedule(int w, int h, const fgm_params* p, int* ow, int* oh, int* oit, int cap) {
+    int n = 0;
+    const int rc = guarded([&] {
+        const auto lv = schedule(w, h, p);
+        n = int(lv.size());
+        for (int l = 0; l < n && l < cap; ++l) {
+            if (ow) ow[l] = lv[size_t(l)].w;
+            if (oh) oh[l] = lv[size_t(l)].h;
+            if (oit) oit[l] = lv[size_t(l)].iters;
+        }
+    });
+    return rc ? -rc : n;
+}
+
+int fgm_ml_solve_f32(const float* image, const float* alpha, int w, int h, const fgm_params* p, float* fg, float* bg,
+                     void* stream) {
+    return guarded([&] {
+        check_dims(w, h);
+        std::vector<ImageIO> io{{image, alpha, w, h, fg, bg, nullptr, nullptr}};
+        solve_batch(io, p, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fgm_ml_solve_levels_f32(const float* image, const float* alpha, int w, int h, const fgm_params* p, float* fg,
+                            float* bg, float* const* level_fg, float* const* level_bg, int n_levels, void* stream) {
+    return guarded([&] {
+        check_dims(w, h);
+        const auto lv = schedule(w, h, p);
+        if (n_levels != int(lv.size()) || !level_fg || !level_bg)
+            throw InvalidArgument("fgm_ml_solve_levels_f32: need one (fg, bg) buffer pair per level (" +
+                                  std::to_string(lv.size()) + ")");
+        std::vector<ImageIO> io{{image, alpha, w, h, fg, bg, level_fg, level_bg}};
+        solve_batch(io, p, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fgm_batch_solve_f32(int n_images, const float* const* images, const float* const* alphas, const int* widths,
+                        const int* heights, const fgm_params* p, float* const* fgs, float* const* bgs, void* stream) {
+    return guarded([&] {
+        if (n_images < 0) throw InvalidArgument("fgm_batch_solve_f32: n_images < 0");
+        if (n_images == 0) return;
+        std::vector<ImageIO> io;
+        io.reserve(size_t(n_images));
+        for (int i = 0; i < n_images; ++i) {
+            check_dims(widths[i], heights[i]);
+            io.push_back({images[i], alphas[i], widths[i], heights[i], fgs[i], bgs[i], nullptr, nullptr});
+        }
+        solve_batch(io, p, static_cast<cudaStream_t>(stream));
+    });
+}
+
+static int host_solve_impl(const void* image, const void* alpha, int w, int h, const fgm_params* p, void* fg,
+                           void* bg, bool f64) {
+    return guarded([&] {
+        check_dims(w, h);
+        validate(p);
+        require_device();
+        cudaStream_t s;
+        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+        struct SG {
+            cudaStream_t s;
+            ~SG() { cudaStreamDestroy(s); }
+        } sg{s};
+        const size_t n = size_t(w) * h;
+        Arena A;
+        A.reserve(al(16 * n * sizeof(float)) + al(24 * n * sizeof(float)) + (f64 ? 2 * al(24 * n * sizeof(double)) : 0),
+                  s);
+        float* dimg = A.take<float>(4 * n);  // 3 image planes + alpha
+        float* dout = A.take<float>(6 * n);
+        if (f64) {
+            double* staging = A.take<double>(6 * n);
+            ck(cudaMemcpyAsync(staging, image, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+            ck(cudaMemcpyAsync(staging + 3 * n, alpha, n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+            ck(launch_f64_to_f32(staging, dimg, 4 * n, s), "f64_to_f32");
+            std::vector<ImageIO> io{{dimg, dimg + 3 * n, w, h, dout, dout + 3 * n, nullptr, nullptr}};
+            solve_batch(io, p, s);
+            double* out64 = A.take<double>(6 * n);
+            ck(launch_f32_to_f64(dout, out64, 6 * n, s), "f32_to_f64");
+            ck(cudaMemcpyAsync(fg, out64, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+            ck(cudaMemcpyAsync(bg, out64 + 3 * n, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+        } else {
+            ck(cudaMemcpyAsync(dimg, image, 3 * n * sizeof(float), cudaMemcpyHostToDevice, s), "H2D");
+            ck(cudaMemcpyAsync(dimg + 3 * n, alpha, n * sizeof(float), cudaMemcpyHostToDevice, s), "H2D");
+            std::vector<ImageIO> io{{dimg, dimg + 3 * n, w, h, dout, dout + 3 * n, nullptr, nullptr}};
+            solve_batch(io, p, s);
+            ck(cudaMemcpyAsync(fg, dout, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, s), "D2H");
+            ck(cudaMemcpyAsync(bg, dout + 3 * n, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, s), "D2H");
+        }
+        ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    });
+}
+
+int fgm_ml_solve_host_f32(const float* image, const float* alpha, int w, int h, const fgm_params* p, float* fg,
+                          float* bg) {
+    return host_solve_impl(image, alpha, w, h, p, fg, bg, false);
+}
+
+int fgm_ml_solve_host_f64(const double* image, const double* alpha, int w, int h, const fgm_params* p, double* fg,
+                          double* bg) {
+    return host_solve_impl(image, alpha, w, h, p, fg, bg, true);
+}
+
+int fgm_resize_f32(const float* src, int sw, int sh, int nplanes, float* dst, int dw, int dh, void* stream) {
+    return guarded([&] {
+        if (dw < 1 || dh < 1)
+            throw InvalidArgument("resize: target size must be >= 1x1, got " + std::to_string(dw) + "x" +
+                                  std::to_string(dh));
+        check_dims(sw, sh);
+        if (nplanes < 1) throw InvalidArgument("resize: nplanes must be >= 1");
+        require_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        Arena A;
+        A.reserve(4096, s);
+        ResampleJob rj{src, dst, sw, sh, dw, dh, nplanes, (long long)sw * sh, (long long)dw * dh};
+        ResampleJob* d = A.take<ResampleJob>(1);
+        ck(cudaMemcpyAsync(d, &rj, sizeof(rj), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
+        ck(launch_resample(d, 1, dh, s), "resample_kernel");
+    });
+}
+
+int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg_in, const float* bg_in, int w,
+                         int h, int iterations, double regularization, double gradient_weight, float* fg_out,
+                         float* bg_out, void* stream) {
+    return guarded([&] {
+        check_dims(w, h);
+        if (iterations < 1) throw InvalidArgument("MlParams: iteration counts must be >= 1");
+        fgm_params p{regularization, gradient_weight, 1, 1, 1};
+        validate(&p);
+        require_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const std::vector<int> ps = passes_for(iterations);
+        const long long px = (long long)w * h;
+        size_t sf = 0;
+        int mb = 0;
+        for (int K : ps) {
+            sf = std::max(sf, sweep_stream_floats(w, h, K));
+            mb = std::max(mb, sweep_bands(h, K));
+        }
+        Arena A;
+        A.reserve(al(sf * 4) + al(size_t(mb + 1) * 4) + 2 * al(6 * size_t(px) * 4) + 256 * (ps.size() + 2), s);
+        float* stream_buf = A.take<float>(sf);
+        unsigned* ctr = A.take<unsigned>(size_t(mb) + 1);
+        float* tmp[2] = {A.take<float>(6 * size_t(px)), A.take<float>(6 * size_t(px))};
+        const float* fi = fg_in;
+        const float* bi = bg_in;
+        for (size_t pi = 0; pi < ps.size(); ++pi) {
+            const bool last = pi + 1 == ps.size();
+            SweepJob J1{};
+            J1.img = image;
+            J1.alpha = alpha;
+            J1.fg_in = fi;
+            J1.bg_in = bi;
+            J1.fg_out = last ? fg_out : tmp[pi & 1];
+            J1.bg_out = last ? bg_out : tmp[pi & 1] + 3 * px;
+            J1.stream = stream_buf;
+            J1.progress = ctr + 1;
+            J1.pstride = px;
+            J1.w = w;
+            J1.h = h;
+            J1.nb = sweep_bands(h, ps[pi]);
+            J1.band_base = 0;
+            ck(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * size_t(J1.nb + 1), s), "memset");
+            SweepJob* d = A.take<SweepJob>(1);
+            ck(cudaMemcpyAsync(d, &J1, sizeof(J1), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
+            {
+                ProfScope pr(s, 0, 64.0 * double(px));
+                ck(launch_sweep(ps[pi], d, 1, J1.nb, ctr, float(regularization), float(gradient_weight), s),
+                   "sweep_kernel");
+            }
+            fi = J1.fg_out;
+            bi = J1.bg_out;
+        }
+    });
+}
+
+void fgm_profile_enable(int on) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof_on = on != 0;
+}
+
+void fgm_profile_reset(void) {
+    prof_drain();
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (int i = 0; i < 3; ++i) {
+        g_launches[i] = 0;
+        g_ms[i] = 0;
+        g_bytes[i] = 0;
+    }
+}
+
+int fgm_kernel_stats(int which, long long* launches, double* ms, double* alg_bytes) {
+    if (which < 0 || which > 2) return FGM_INVALID_ARGUMENT;
+    prof_drain();
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (launches) *launches = g_launches[which];
+    if (ms) *ms = g_ms[which];
+    if (alg_bytes) *alg_bytes = g_bytes[which];
+    return FGM_OK;
+}
+
+const char* fgm_last_error(void) { return fgm::g_err.c_str(); }
+
+int fgm_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+const char* fgm_version(void) { return "fgmatte_b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"
