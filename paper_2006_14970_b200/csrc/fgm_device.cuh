@@ -16,8 +16,9 @@ struct Tap {
     float t;
 };
 
-__device__ __forceinline__ Tap make_tap(int d, int src, int dst) {
-    const double scale = __ddiv_rn(double(src), double(dst));
+// `scale` must be double(src) / double(dst), rounded (computed once per
+// axis on the host, or by make_tap below).
+__device__ __forceinline__ Tap make_tap_s(int d, int src, double scale) {
     double f = __dadd_rn(__dmul_rn(__dadd_rn(double(d), 0.5), scale), -0.5);
     if (f < 0.0) f = 0.0;
     const double max_f = double(src - 1);
@@ -28,6 +29,10 @@ __device__ __forceinline__ Tap make_tap(int d, int src, int dst) {
     tp.i1 = min(i0 + 1, src - 1);
     tp.t = float(__dadd_rn(f, -double(i0)));
     return tp;
+}
+
+__device__ __forceinline__ Tap make_tap(int d, int src, int dst) {
+    return make_tap_s(d, src, __ddiv_rn(double(src), double(dst)));
 }
 
 // Two-stage lerp as resize_plane (image.cpp:98-102): horizontal on both rows,
@@ -44,49 +49,110 @@ __device__ __forceinline__ float edge_weight(float ai, float aj, float eps, floa
 }
 
 // The per-pixel system of multilevel.cpp:94-118 (PixelSystem,
-// multilevel.hpp:45-75), solved in a cancellation-free form.  With
-// u = (a, 1-a), S = sum_j d_j, SF_c = sum_j d_j F_j,c, SB_c likewise,
-// m = S^-1 * (SF, SB), the reference's adj(A) b / det(A) equals
-//   F_c = (u1 (u1 mF - u0 mB) + u0 I_c + SF_c) / (u0^2 + u1^2 + S)
-//   B_c = (u0 (u0 mB - u1 mF) + u1 I_c + SB_c) / (u0^2 + u1^2 + S)
-// exactly in real arithmetic (det = S (u0^2 + u1^2 + S)).  In fp32 the
-// reference's form loses ~log10(1/S) digits to cancellation (2e-3 max error at
-// eps_r = 1e-5 on a 1x1 image); this form stays within a few ulps.  Every
-// operation is written index-symmetrically in (F, B) / (u0, u1), so
-// complementing alpha swaps the outputs bitwise (test_multilevel.cpp:167-180).
-// Neighbour order L, R, U, D as multilevel.cpp:104-105.
-struct PixelIn {
-    float a, aL, aR, aU, aD;
-    float I[3];
+// multilevel.hpp:45-75).  With u = (a, 1-a), d_j = eps + omega |a - a_j| over
+// the clamped neighbours L, R, U, D (multilevel.cpp:104-106), S = sum d_j and
+// D = u0^2 + u1^2 + S, the reference's adj(A) b / det(A) (det = S D) equals
+//   F_c = A  SF_c + Bc SB_c + (u0/D) I_c,   A  = (1 + u1^2/S) / D
+//   B_c = A' SB_c + Bc SF_c + (u1/D) I_c,   A' = (1 + u0^2/S) / D,  Bc = -u0 u1 / (S D)
+// with SF_c = sum_j d_j F_j,c (likewise SB_c).  The reference's form
+// (diag1 rhs0 - off rhs1) / det cancels catastrophically in fp32 when S is
+// small (2e-3 max error at eps_r = 1e-5 on a 1x1 image); this one has no
+// cancellation beyond the data's own and stays within a few ulps of fp64.
+// The alpha-only coefficients (Coef) are computed once per pixel; the
+// neighbour part costs 4 FMAs per sum and 2 per output.  Every operation is
+// mirrored in (F, B) / (u0, u1), so complementing alpha swaps the outputs
+// bitwise (test_multilevel.cpp:167-180).  A clamped (missing) neighbour is
+// passed as a_j = a, giving d_j = eps exactly as the reference's self term.
+struct Coef {
+    float dL, dR, dU, dD, A, A2, Bc, pI[3], qI[3];
 };
 
-__device__ __forceinline__ void solve_pixel(const PixelIn& p, const float* L, const float* R, const float* U,
-                                            const float* D, float eps, float omega, float* out) {
-    const float dL = edge_weight(p.a, p.aL, eps, omega);
-    const float dR = edge_weight(p.a, p.aR, eps, omega);
-    const float dU = edge_weight(p.a, p.aU, eps, omega);
-    const float dD = edge_weight(p.a, p.aD, eps, omega);
-    const float S = __fadd_rn(__fadd_rn(__fadd_rn(dL, dR), dU), dD);
-    const float u0 = p.a;
-    const float u1 = __fsub_rn(1.0f, p.a);
-    const float iS = __frcp_rn(S);
-    const float iD = __frcp_rn(__fadd_rn(__fadd_rn(__fmul_rn(u0, u0), __fmul_rn(u1, u1)), S));
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ Coef pixel_coef(float a, float aL, float aR, float aU, float aD, const float* I,
+                                           float eps, float omega) {
+    Coef co;
+    co.dL = edge_weight(a, aL, eps, omega);
+    co.dR = edge_weight(a, aR, eps, omega);
+    co.dU = edge_weight(a, aU, eps, omega);
+    co.dD = edge_weight(a, aD, eps, omega);
+    const float S = __fadd_rn(__fadd_rn(__fadd_rn(co.dL, co.dR), co.dU), co.dD);
+    const float u0 = a, u1 = __fsub_rn(1.0f, a);
+    const float u00 = __fmul_rn(u0, u0), u11 = __fmul_rn(u1, u1), u01 = __fmul_rn(u0, u1);
+    const float iS = rcp_approx(S);
+    const float iD = rcp_approx(__fadd_rn(__fadd_rn(u00, u11), S));
+    co.A = __fmul_rn(iD, __fmaf_rn(u11, iS, 1.0f));
+    co.A2 = __fmul_rn(iD, __fmaf_rn(u00, iS, 1.0f));
+    co.Bc = -__fmul_rn(iD, __fmul_rn(u01, iS));
+    const float p = __fmul_rn(iD, u0), qq = __fmul_rn(iD, u1);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        float SF = __fmul_rn(dL, L[c]);
-        float SB = __fmul_rn(dL, L[3 + c]);
-        SF = __fmaf_rn(dR, R[c], SF);
-        SB = __fmaf_rn(dR, R[3 + c], SB);
-        SF = __fmaf_rn(dU, U[c], SF);
-        SB = __fmaf_rn(dU, U[3 + c], SB);
-        SF = __fmaf_rn(dD, D[c], SF);
-        SB = __fmaf_rn(dD, D[3 + c], SB);
-        const float mF = __fmul_rn(SF, iS);
-        const float mB = __fmul_rn(SB, iS);
-        const float tF = __fmaf_rn(u1, mF, -__fmul_rn(u0, mB));
-        const float tB = __fmaf_rn(u0, mB, -__fmul_rn(u1, mF));
-        out[c] = __saturatef(__fmul_rn(__fmaf_rn(u1, tF, __fmaf_rn(u0, p.I[c], SF)), iD));
-        out[3 + c] = __saturatef(__fmul_rn(__fmaf_rn(u0, tB, __fmaf_rn(u1, p.I[c], SB)), iD));
+        co.pI[c] = __fmul_rn(p, I[c]);
+        co.qI[c] = __fmul_rn(qq, I[c]);
+    }
+    return co;
+}
+
+// Single-channel variants (one colour channel c; the sweep kernel runs the
+// three channels in separate warps).
+struct Coef1 {
+    float dL, dR, dU, dD, A, A2, Bc, pI, qI;
+};
+
+__device__ __forceinline__ Coef1 pixel_coef1(float a, float aL, float aR, float aU, float aD, float I, float eps,
+                                             float omega) {
+    Coef1 co;
+    co.dL = edge_weight(a, aL, eps, omega);
+    co.dR = edge_weight(a, aR, eps, omega);
+    co.dU = edge_weight(a, aU, eps, omega);
+    co.dD = edge_weight(a, aD, eps, omega);
+    const float S = __fadd_rn(__fadd_rn(__fadd_rn(co.dL, co.dR), co.dU), co.dD);
+    const float u0 = a, u1 = __fsub_rn(1.0f, a);
+    const float u00 = __fmul_rn(u0, u0), u11 = __fmul_rn(u1, u1), u01 = __fmul_rn(u0, u1);
+    const float iS = rcp_approx(S);
+    const float iD = rcp_approx(__fadd_rn(__fadd_rn(u00, u11), S));
+    co.A = __fmul_rn(iD, __fmaf_rn(u11, iS, 1.0f));
+    co.A2 = __fmul_rn(iD, __fmaf_rn(u00, iS, 1.0f));
+    co.Bc = -__fmul_rn(iD, __fmul_rn(u01, iS));
+    co.pI = __fmul_rn(__fmul_rn(iD, u0), I);
+    co.qI = __fmul_rn(__fmul_rn(iD, u1), I);
+    return co;
+}
+
+// (x, y) = (F_c, B_c) of the four neighbours; returns the new (F_c, B_c).
+__device__ __forceinline__ float2 pixel_apply1(const Coef1& co, float2 L, float2 R, float2 U, float2 D) {
+    float SF = __fmul_rn(co.dL, L.x);
+    float SB = __fmul_rn(co.dL, L.y);
+    SF = __fmaf_rn(co.dD, D.x, SF);
+    SB = __fmaf_rn(co.dD, D.y, SB);
+    SF = __fmaf_rn(co.dR, R.x, SF);
+    SB = __fmaf_rn(co.dR, R.y, SB);
+    SF = __fmaf_rn(co.dU, U.x, SF);
+    SB = __fmaf_rn(co.dU, U.y, SB);
+    return make_float2(__saturatef(__fmaf_rn(co.A, SF, __fmaf_rn(co.Bc, SB, co.pI))),
+                       __saturatef(__fmaf_rn(co.A2, SB, __fmaf_rn(co.Bc, SF, co.qI))));
+}
+
+// Neighbour-dependent part.  Values from this lane's previous step (L, D)
+// enter first, shuffled ones (R, U) last, to keep the recurrence short.
+__device__ __forceinline__ void pixel_apply(const Coef& co, const float* L, const float* R, const float* U,
+                                            const float* D, float* out) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        float SF = __fmul_rn(co.dL, L[c]);
+        float SB = __fmul_rn(co.dL, L[3 + c]);
+        SF = __fmaf_rn(co.dD, D[c], SF);
+        SB = __fmaf_rn(co.dD, D[3 + c], SB);
+        SF = __fmaf_rn(co.dR, R[c], SF);
+        SB = __fmaf_rn(co.dR, R[3 + c], SB);
+        SF = __fmaf_rn(co.dU, U[c], SF);
+        SB = __fmaf_rn(co.dU, U[3 + c], SB);
+        out[c] = __saturatef(__fmaf_rn(co.A, SF, __fmaf_rn(co.Bc, SB, co.pI[c])));
+        out[3 + c] = __saturatef(__fmaf_rn(co.A2, SB, __fmaf_rn(co.Bc, SF, co.qI[c])));
     }
 }
 

@@ -12,6 +12,7 @@ struct ResampleJob {
     float* dst;
     int sw, sh, dw, dh, nplanes;
     long long spstride, dpstride;  // plane strides in floats
+    double sx, sy;                 // double(sw)/double(dw), double(sh)/double(dh) (image.cpp:73)
 };
 
 // ---- K4: coarse levels, one CTA per image, shared-memory resident ---------
@@ -32,8 +33,7 @@ struct CoarseJob {
 
 // ---- K3: big-level sweep, skewed-band wavefront ---------------------------
 constexpr int kBandRows = 32;   // one warp = 32 skewed rows
-constexpr int kChunk = 32;      // boundary-stream publication granularity (columns)
-constexpr int kWarpsPerCta = 4;
+constexpr int kChunk = 16;      // boundary-stream publication granularity (columns)
 
 struct SweepJob {
     const float* img;    // 3 planes
@@ -42,25 +42,34 @@ struct SweepJob {
     const float* bg_in;
     float* fg_out;
     float* bg_out;
-    float* stream;       // nb * (w + K - 1) * K * 6 floats
-    unsigned* progress;  // nb counters (zeroed before launch)
+    float* stream;       // 3 * nb streams of sweep_stream_len(w, K) floats
+    unsigned* progress;  // 3 * nb counters (zeroed before launch)
     long long pstride;   // w*h
     int w, h, nb, band_base;
+    int vec4;            // rows are 16-byte aligned (w % 4 == 0, aligned bases): 16-byte cp.async
 };
 
+// A job of one sweep launch is split into (band, channel) work items: band q,
+// channel c has stream / counter index 3q + c.  A stream holds, per skewed
+// column u, the K (F_c, B_c) pairs of the band's last row, padded to 16 bytes.
 inline int sweep_bands(int h, int K) { return (h + K - 1 + kBandRows - 1) / kBandRows; }
+__host__ __device__ inline size_t sweep_stream_len(int w, int K) {
+    return (size_t(w + K - 1) * size_t(K) * 2 + 3) / 4 * 4;
+}
 inline size_t sweep_stream_floats(int w, int h, int K) {
-    return size_t(sweep_bands(h, K)) * size_t(w + K - 1) * size_t(K) * 6;
+    return size_t(sweep_bands(h, K)) * 3 * sweep_stream_len(w, K);
 }
 
 // Launch helpers (kernels.cu).  `jobs_dev` are device copies of the arrays.
 cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long max_px, cudaStream_t s);
 cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float omega, cudaStream_t s);
-cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, int njobs, int total_bands, unsigned* ticket, float eps,
-                         float omega, cudaStream_t s);
+// order_dev[t] = (job, 3 * band + channel) of ticket t, band-major across jobs.
+cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands, unsigned* ticket,
+                         float eps, float omega, cudaStream_t s);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);
 cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s);
 size_t coarse_smem_bytes();
 int sweep_supported_k(int K);  // 1 if a K-template exists
+size_t sweep_smem_bytes(int K);
 
 }  // namespace fgm

@@ -3,9 +3,7 @@
 //   K1/K2 resample_kernel  -- bilinear level resampling (image.cpp:71-133)
 //   K4    coarse_kernel    -- all coarse levels of an image in one CTA, in
 //                             shared memory, exact Gauss-Seidel order
-//   K3    sweep_kernel<K>  -- K fused in-place scanline sweeps of one big level
-//                             (multilevel.cpp:81-121 x iterations), as a
-//                             skewed-band wavefront across warps / CTAs
+//   (K3, the big-level sweep, lives in sweep.cu)
 //
 // See DESIGN.md for the dependency analysis that makes K3 exact.
 #include <cuda_runtime.h>
@@ -32,9 +30,9 @@ __global__ void __launch_bounds__(256) resample_kernel(const ResampleJob* __rest
             }
             continue;
         }
-        const Tap ty = make_tap(y, J.sh, J.dh);
+        const Tap ty = make_tap_s(y, J.sh, J.sy);
         for (int x = threadIdx.x; x < J.dw; x += blockDim.x) {
-            const Tap tx = make_tap(x, J.sw, J.dw);
+            const Tap tx = make_tap_s(x, J.sw, J.sx);
             const long long r0 = (long long)ty.i0 * J.sw, r1 = (long long)ty.i1 * J.sw;
             const long long o = (long long)y * J.dw + x;
             for (int p = 0; p < J.nplanes; ++p) {
@@ -71,15 +69,11 @@ __device__ __forceinline__ void coarse_update(float* __restrict__ sI, float* __r
     const int i = y * w + x;
     const int jL = x > 0 ? i - 1 : i, jR = x < w - 1 ? i + 1 : i;
     const int jU = y > 0 ? i - w : i, jD = y < h - 1 ? i + w : i;
-    PixelIn P;
-    P.a = sA[i];
-    P.aL = sA[jL];
-    P.aR = sA[jR];
-    P.aU = sA[jU];
-    P.aD = sA[jD];
+    float I[3];
     float L[6], R[6], U[6], D[6], out[6];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) P.I[c] = sI[c * n + i];
+    for (int c = 0; c < 3; ++c) I[c] = sI[c * n + i];
+    const Coef co = pixel_coef(sA[i], sA[jL], sA[jR], sA[jU], sA[jD], I, eps, omega);
 #pragma unroll
     for (int p = 0; p < 6; ++p) {
         L[p] = fb[p * n + jL];
@@ -87,7 +81,7 @@ __device__ __forceinline__ void coarse_update(float* __restrict__ sI, float* __r
         U[p] = fb[p * n + jU];
         D[p] = fb[p * n + jD];
     }
-    solve_pixel(P, L, R, U, D, eps, omega, out);
+    pixel_apply(co, L, R, U, D, out);
 #pragma unroll
     for (int p = 0; p < 6; ++p) fb[p * n + i] = out[p];
 }
@@ -111,6 +105,8 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_kernel(const CoarseJob*
         const float* prv = sFB[(l & 1) ^ 1];
         const bool ident = (w == W && h == H);
         const bool same = (w == pw && h == ph);
+        const double sxf = __ddiv_rn(double(W), double(w)), syf = __ddiv_rn(double(H), double(h));
+        const double sxp = __ddiv_rn(double(pw), double(w)), syp = __ddiv_rn(double(ph), double(h));
         for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
             const int y = idx / w, x = idx - y * w;
             if (ident) {  // the last level resamples the original: identity copy
@@ -118,7 +114,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_kernel(const CoarseJob*
                 for (int c = 0; c < 3; ++c) sI[c * n + idx] = J.img[c * fps + idx];
                 sA[idx] = J.alpha[idx];
             } else {
-                const Tap tx = make_tap(x, W, w), ty = make_tap(y, H, h);
+                const Tap tx = make_tap_s(x, W, sxf), ty = make_tap_s(y, H, syf);
                 const long long r0 = (long long)ty.i0 * W, r1 = (long long)ty.i1 * W;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -138,7 +134,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_kernel(const CoarseJob*
 #pragma unroll
                 for (int p = 0; p < 6; ++p) cur[p * n + idx] = prv[p * pn + idx];
             } else {
-                const Tap tx = make_tap(x, pw, w), ty = make_tap(y, ph, h);
+                const Tap tx = make_tap_s(x, pw, sxp), ty = make_tap_s(y, ph, syp);
                 const int r0 = ty.i0 * pw, r1 = ty.i1 * pw;
 #pragma unroll
                 for (int p = 0; p < 6; ++p) {
@@ -186,236 +182,6 @@ cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float
     }
     coarse_kernel<<<njobs, kCoarseThreads, coarse_smem_bytes(), s>>>(jobs_dev, eps, omega);
     return cudaGetLastError();
-}
-
-// ============================================================================
-// K3: big-level sweeps.
-//
-// Skewed coordinates u = x + k, v = y + k turn every dependency of the
-// in-place scanline Gauss-Seidel (L, U new; R, D, self old) into a
-// non-negative (du, dv) step, so bands of 32 skewed rows depend only on the
-// band above.  Lane j of a warp owns skewed row v = 32q + j; at step t it
-// updates, for every sweep k < K, pixel (x, y) = (t - v - k, v - k).  All
-// neighbour values come from the lane itself or from lane j-1 one step
-// earlier (registers + shfl).  Lane 0 gets lane "-1" (the band above) from
-// that band's boundary stream in global memory, published every kChunk
-// columns with release/acquire counters.  Bands are handed out by an atomic
-// ticket in dependency order, so every awaited band is already running.
-// ============================================================================
-template <int K>
-__device__ __forceinline__ void run_band(const SweepJob& J, int q, int lane, float* __restrict__ chunk, float eps,
-                                         float omega) {
-    const int w = J.w, h = J.h;
-    const int Umax = w + K - 1;
-    const int v = q * kBandRows + lane;
-    const long long ps = J.pstride;
-    const float* __restrict__ A = J.alpha;
-    const float* __restrict__ IM = J.img;
-    const float* __restrict__ FI = J.fg_in;
-    const float* __restrict__ BI = J.bg_in;
-    float* __restrict__ FO = J.fg_out;
-    float* __restrict__ BO = J.bg_out;
-    const size_t slen = size_t(Umax) * K * 6;
-    const float* up_stream = q > 0 ? J.stream + size_t(q - 1) * slen : nullptr;
-    float* my_stream = J.stream + size_t(q) * slen;
-    const bool has_down = q < J.nb - 1;
-    const bool vrow = v < h;
-
-    float outp[K][6], rprev[K][6];
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int c = 0; c < 6; ++c) outp[k][c] = rprev[k][c] = 0.0f;
-    float fbR[6], fbS[6];
-#pragma unroll
-    for (int c = 0; c < 6; ++c) fbR[c] = fbS[c] = 0.0f;
-    float aR = 0.0f, aS = 0.0f, aL = 0.0f;
-
-    const int tbeg = q * kBandRows - 1;
-    const int tend = q * kBandRows + (kBandRows - 1) + Umax;
-    for (int t = tbeg; t < tend; ++t) {
-        const int u = t - v;
-        const int u0 = t - q * kBandRows;  // lane 0's column
-        if (q > 0 && u0 >= 0 && u0 < Umax && (u0 % kChunk) == 0) {
-            const int need = min(u0 + kChunk, Umax);
-            while (ld_acquire(J.progress + (q - 1)) < unsigned(need)) __nanosleep(32);
-            __syncwarp();
-            const int nfl = (need - u0) * K * 6;
-            const float* src = up_stream + size_t(u0) * K * 6;
-            for (int e = lane; e < nfl; e += 32) chunk[e] = __ldcg(src + e);
-            __syncwarp();
-        }
-        // values of lane j-1 from step t-1: U of sweep k, R of sweep k+1
-        float recv[K][6];
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-#pragma unroll
-            for (int c = 0; c < 6; ++c) recv[k][c] = __shfl_up_sync(kFull, outp[k][c], 1);
-        if (lane == 0) {
-            const bool ok = q > 0 && u0 >= 0 && u0 < Umax;
-            const float* src = chunk + (ok ? (u0 % kChunk) * K * 6 : 0);
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-#pragma unroll
-                for (int c = 0; c < 6; ++c) recv[k][c] = ok ? src[k * 6 + c] : 0.0f;
-        }
-        // sweep 0 reads the pass input: slide (u, v) <- (u+1, v)
-#pragma unroll
-        for (int c = 0; c < 6; ++c) fbS[c] = fbR[c];
-        aL = aS;
-        aS = aR;
-        {
-            const int x1 = u + 1;
-            if (vrow && x1 >= 0 && x1 < w) {
-                const long long idx = (long long)v * w + x1;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    fbR[c] = __ldg(FI + c * ps + idx);
-                    fbR[3 + c] = __ldg(BI + c * ps + idx);
-                }
-                aR = __ldg(A + idx);
-            } else {
-#pragma unroll
-                for (int c = 0; c < 6; ++c) fbR[c] = 0.0f;
-                aR = 0.0f;
-            }
-        }
-        float fbD0[6];
-#pragma unroll
-        for (int c = 0; c < 6; ++c) fbD0[c] = __shfl_down_sync(kFull, fbR[c], 1);
-        float aD0 = __shfl_down_sync(kFull, aR, 1);
-        float aU0 = __shfl_up_sync(kFull, aL, 1);
-        if (lane == kBandRows - 1 && v + 1 < h && u >= 0 && u < w) {
-            const long long idx = (long long)(v + 1) * w + u;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                fbD0[c] = __ldg(FI + c * ps + idx);
-                fbD0[3 + c] = __ldg(BI + c * ps + idx);
-            }
-            aD0 = __ldg(A + idx);
-        }
-        if (lane == 0 && v >= 1 && v - 1 < h && u >= 0 && u < w) aU0 = __ldg(A + (long long)(v - 1) * w + u);
-
-        float nv[K][6];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int x = u - k, y = v - k;
-            const bool act = x >= 0 && x < w && y >= 0 && y < h;
-            if (act) {
-                const long long idx = (long long)y * w + x;
-                PixelIn P;
-                float self[6], L[6], R[6], U[6], D[6];
-#pragma unroll
-                for (int c = 0; c < 6; ++c) self[c] = k == 0 ? fbS[c] : rprev[k > 0 ? k - 1 : 0][c];
-                if (k == 0) {
-                    P.a = aS;
-                    P.aL = x > 0 ? aL : aS;
-                    P.aR = x < w - 1 ? aR : aS;
-                    P.aU = y > 0 ? aU0 : aS;
-                    P.aD = y < h - 1 ? aD0 : aS;
-                } else {
-                    P.a = __ldg(A + idx);
-                    P.aL = x > 0 ? __ldg(A + idx - 1) : P.a;
-                    P.aR = x < w - 1 ? __ldg(A + idx + 1) : P.a;
-                    P.aU = y > 0 ? __ldg(A + idx - w) : P.a;
-                    P.aD = y < h - 1 ? __ldg(A + idx + w) : P.a;
-                }
-#pragma unroll
-                for (int c = 0; c < 3; ++c) P.I[c] = __ldg(IM + c * ps + idx);
-#pragma unroll
-                for (int c = 0; c < 6; ++c) {
-                    L[c] = x > 0 ? outp[k][c] : self[c];
-                    R[c] = x < w - 1 ? (k == 0 ? fbR[c] : recv[k > 0 ? k - 1 : 0][c]) : self[c];
-                    U[c] = y > 0 ? recv[k][c] : self[c];
-                    D[c] = y < h - 1 ? (k == 0 ? fbD0[c] : outp[k > 0 ? k - 1 : 0][c]) : self[c];
-                }
-                solve_pixel(P, L, R, U, D, eps, omega, nv[k]);
-                if (k == K - 1) {
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        FO[c * ps + idx] = nv[k][c];
-                        BO[c * ps + idx] = nv[k][3 + c];
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int c = 0; c < 6; ++c) nv[k][c] = 0.0f;
-            }
-        }
-        if (lane == kBandRows - 1 && has_down && u >= 0 && u < Umax) {
-            float* dst = my_stream + size_t(u) * K * 6;
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-#pragma unroll
-                for (int c = 0; c < 6; ++c) dst[k * 6 + c] = nv[k][c];
-            if (((u + 1) % kChunk) == 0 || u + 1 == Umax) {
-                __threadfence();
-                st_release(J.progress + q, unsigned(u + 1));
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-#pragma unroll
-            for (int c = 0; c < 6; ++c) {
-                rprev[k][c] = recv[k][c];
-                outp[k][c] = nv[k][c];
-            }
-    }
-}
-
-template <int K>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) sweep_kernel(const SweepJob* __restrict__ jobs, int njobs,
-                                                                   int total_bands, unsigned* ticket, float eps,
-                                                                   float omega) {
-    __shared__ float chunks[kWarpsPerCta][kChunk * K * 6];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (;;) {
-        unsigned tk = 0;
-        if (lane == 0) tk = atomicAdd(ticket, 1u);
-        tk = __shfl_sync(kFull, tk, 0);
-        if (tk >= unsigned(total_bands)) return;
-        int lo = 0, hi = njobs - 1;  // last job with band_base <= tk
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (unsigned(jobs[mid].band_base) <= tk)
-                lo = mid;
-            else
-                hi = mid - 1;
-        }
-        const SweepJob J = jobs[lo];
-        run_band<K>(J, int(tk) - J.band_base, lane, chunks[warp], eps, omega);
-    }
-}
-
-template <int K>
-static cudaError_t launch_sweep_k(const SweepJob* jobs_dev, int njobs, int total_bands, unsigned* ticket, float eps,
-                                  float omega, cudaStream_t s) {
-    static int grid_cap = 0;
-    if (grid_cap == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<K>, kWarpsPerCta * 32, 0);
-        grid_cap = std::max(1, sms * std::max(1, per_sm));
-    }
-    const int want = (total_bands + kWarpsPerCta - 1) / kWarpsPerCta;
-    const int grid = std::max(1, std::min(want, grid_cap));
-    sweep_kernel<K><<<grid, kWarpsPerCta * 32, 0, s>>>(jobs_dev, njobs, total_bands, ticket, eps, omega);
-    return cudaGetLastError();
-}
-
-int sweep_supported_k(int K) { return K == 1 || K == 2 || K == 3 || K == 4 || K == 8; }
-
-cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, int njobs, int total_bands, unsigned* ticket, float eps,
-                         float omega, cudaStream_t s) {
-    switch (K) {
-        case 1: return launch_sweep_k<1>(jobs_dev, njobs, total_bands, ticket, eps, omega, s);
-        case 2: return launch_sweep_k<2>(jobs_dev, njobs, total_bands, ticket, eps, omega, s);
-        case 3: return launch_sweep_k<3>(jobs_dev, njobs, total_bands, ticket, eps, omega, s);
-        case 4: return launch_sweep_k<4>(jobs_dev, njobs, total_bands, ticket, eps, omega, s);
-        case 8: return launch_sweep_k<8>(jobs_dev, njobs, total_bands, ticket, eps, omega, s);
-        default: return cudaErrorInvalidValue;
-    }
 }
 
 // ============================================================================

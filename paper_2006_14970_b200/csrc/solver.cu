@@ -80,7 +80,7 @@ std::vector<Level> schedule(int W, int H, const fgm_params* p) {
 
 // Split `iters` sweeps into fused passes with a compiled K.
 std::vector<int> passes_for(int iters) {
-    static const int ks[] = {8, 4, 3, 2, 1};
+    static const int ks[] = {4, 3, 2, 1};
     std::vector<int> out;
     while (iters > 0) {
         for (int k : ks)
@@ -163,6 +163,28 @@ void require_device() {
         }
         pool_set = true;
     }
+}
+
+ResampleJob rjob(const float* src, float* dst, int sw, int sh, int dw, int dh, int np) {
+    ResampleJob r{};
+    r.src = src;
+    r.dst = dst;
+    r.sw = sw;
+    r.sh = sh;
+    r.dw = dw;
+    r.dh = dh;
+    r.nplanes = np;
+    r.spstride = (long long)sw * sh;
+    r.dpstride = (long long)dw * dh;
+    r.sx = double(sw) / double(dw);  // make_taps' scale, image.cpp:73
+    r.sy = double(sh) / double(dh);
+    return r;
+}
+
+// 16-byte cp.async needs every row start 16-byte aligned.
+int vec4_ok(const SweepJob& j) {
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    return (j.w % 4 == 0) && al16(j.img) && al16(j.alpha) && al16(j.fg_in) && al16(j.bg_in) ? 1 : 0;
 }
 
 // ---- stream-ordered workspace ----------------------------------------------
@@ -270,11 +292,25 @@ struct JobStage {
     }
 };
 
+// Ticket order of a sweep launch: band-major across its jobs, so that the
+// bands running at any moment belong to many images (no pipeline fill per
+// image) and every band's predecessor has a smaller ticket.
+std::vector<int2> band_order(const std::vector<SweepJob>& sj) {
+    int maxnb = 0;
+    for (const auto& j : sj) maxnb = std::max(maxnb, j.nb);
+    std::vector<int2> ord;
+    for (int q = 0; q < maxnb; ++q)
+        for (size_t i = 0; i < sj.size(); ++i)
+            if (q < sj[i].nb)
+                for (int c = 0; c < 3; ++c) ord.push_back(make_int2(int(i), 3 * q + c));
+    return ord;
+}
+
 enum LaunchKind { kCoarse, kResample, kSweep, kCopy };
 struct LaunchRec {
     LaunchKind kind;
     int K, njobs, total_bands;
-    size_t job_off, ticket;
+    size_t job_off, ticket, order_off;
     long long max_rows;
     double bytes;
     void* dst = nullptr;
@@ -336,7 +372,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             }
             bytes += 24.0 * double(n);
         }
-        launches.push_back({kCoarse, 0, int(cj.size()), 0, st.push(cj), 0, 0, bytes});
+        launches.push_back({kCoarse, 0, int(cj.size()), 0, st.push(cj), 0, 0, 0, bytes});
     }
 
     // ---- big levels, aligned so that every image's top level is step J-1 --
@@ -358,20 +394,20 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             const long long px = (long long)L.w * L.h, ppx = (long long)Lp.w * Lp.h;
             const long long fpx = (long long)P.io.W * P.io.H;
             if (l < n - 1) {
-                rj.push_back({P.io.img, P.lvlIA, P.io.W, P.io.H, L.w, L.h, 3, fpx, px});
-                rj.push_back({P.io.alpha, P.lvlIA + 3 * px, P.io.W, P.io.H, L.w, L.h, 1, fpx, px});
+                rj.push_back(rjob(P.io.img, P.lvlIA, P.io.W, P.io.H, L.w, L.h, 3));
+                rj.push_back(rjob(P.io.alpha, P.lvlIA + 3 * px, P.io.W, P.io.H, L.w, L.h, 1));
                 rbytes += 4.0 * 4 * (double(px) + std::min<double>(double(fpx), 4.0 * px));
             }
-            rj.push_back({P.fbOut, P.fbInit, Lp.w, Lp.h, L.w, L.h, 6, ppx, px});
+            rj.push_back(rjob(P.fbOut, P.fbInit, Lp.w, Lp.h, L.w, L.h, 6));
             rbytes += 4.0 * 6 * (double(px) + double(ppx));
             max_rows = std::max<long long>(max_rows, L.h);
         }
         if (act.empty()) continue;
-        launches.push_back({kResample, 0, int(rj.size()), 0, st.push(rj), 0, max_rows, rbytes});
+        launches.push_back({kResample, 0, int(rj.size()), 0, st.push(rj), 0, 0, max_rows, rbytes});
         size_t max_passes = 0;
         for (auto& a : act) max_passes = std::max(max_passes, passes_for(a.P->lv[size_t(a.l)].iters).size());
         for (size_t pi = 0; pi < max_passes; ++pi) {
-            for (int K : {8, 4, 3, 2, 1}) {
+            for (int K : {4, 3, 2, 1}) {
                 std::vector<SweepJob> sj;
                 int total = 0;
                 double sbytes = 0;
@@ -405,9 +441,10 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                     J1.h = L.h;
                     J1.nb = sweep_bands(L.h, K);
                     J1.band_base = total;
+                    J1.vec4 = vec4_ok(J1);
                     J1.progress = reinterpret_cast<unsigned*>(uintptr_t(st.counters));  // patched below
-                    st.counters += size_t(J1.nb);
-                    total += J1.nb;
+                    st.counters += 3 * size_t(J1.nb);
+                    total += 3 * J1.nb;
                     sbytes += 64.0 * double(px);
                     sj.push_back(J1);
                 }
@@ -417,7 +454,8 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 }
                 const size_t off = st.push(sj);
                 for (size_t k = 0; k < sj.size(); ++k) st.sweep_offsets.push_back(off + k * sizeof(SweepJob));
-                launches.push_back({kSweep, K, int(sj.size()), total, off, ticket, 0, sbytes});
+                const size_t ooff = st.push(band_order(sj));
+                launches.push_back({kSweep, K, int(sj.size()), total, off, ticket, ooff, 0, sbytes});
             }
         }
         for (auto& a : act) {  // per-level dumps (debug API)
@@ -429,9 +467,9 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             const float* f = top ? P.io.fg : P.fbOut;
             const float* b = top ? P.io.bg : P.fbOut + 3 * px;
             if (P.io.level_fg[a.l])
-                launches.push_back({kCopy, 0, 0, 0, 0, 0, 0, double(3 * px * sizeof(float)), P.io.level_fg[a.l], f});
+                launches.push_back({kCopy, 0, 0, 0, 0, 0, 0, 0, double(3 * px * sizeof(float)), P.io.level_fg[a.l], f});
             if (P.io.level_bg[a.l])
-                launches.push_back({kCopy, 0, 0, 0, 0, 0, 0, double(3 * px * sizeof(float)), P.io.level_bg[a.l], b});
+                launches.push_back({kCopy, 0, 0, 0, 0, 0, 0, 0, double(3 * px * sizeof(float)), P.io.level_bg[a.l], b});
         }
     }
 
@@ -462,8 +500,9 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             }
             case kSweep: {
                 ProfScope ps(s, 0, r.bytes);
-                ck(launch_sweep(r.K, reinterpret_cast<const SweepJob*>(djobs + r.job_off), r.njobs, r.total_bands,
-                                dctr + r.ticket, eps, omega, s),
+                ck(launch_sweep(r.K, reinterpret_cast<const SweepJob*>(djobs + r.job_off),
+                                reinterpret_cast<const int2*>(djobs + r.order_off), r.total_bands, dctr + r.ticket, eps,
+                                omega, s),
                    "sweep_kernel");
                 break;
             }
@@ -626,7 +665,7 @@ int fgm_resize_f32(const float* src, int sw, int sh, int nplanes, float* dst, in
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         Arena A;
         A.reserve(4096, s);
-        ResampleJob rj{src, dst, sw, sh, dw, dh, nplanes, (long long)sw * sh, (long long)dw * dh};
+        ResampleJob rj = rjob(src, dst, sw, sh, dw, dh, nplanes);
         ResampleJob* d = A.take<ResampleJob>(1);
         ck(cudaMemcpyAsync(d, &rj, sizeof(rj), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
         ck(launch_resample(d, 1, dh, s), "resample_kernel");
@@ -652,9 +691,10 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
             mb = std::max(mb, sweep_bands(h, K));
         }
         Arena A;
-        A.reserve(al(sf * 4) + al(size_t(mb + 1) * 4) + 2 * al(6 * size_t(px) * 4) + 256 * (ps.size() + 2), s);
+        A.reserve(al(sf * 4) + al(size_t(3 * mb + 1) * 4) + 2 * al(6 * size_t(px) * 4) + 256 * (ps.size() + 2) +
+                      al(size_t(3 * mb) * sizeof(int2)) * ps.size(), s);
         float* stream_buf = A.take<float>(sf);
-        unsigned* ctr = A.take<unsigned>(size_t(mb) + 1);
+        unsigned* ctr = A.take<unsigned>(size_t(3 * mb) + 1);
         float* tmp[2] = {A.take<float>(6 * size_t(px)), A.take<float>(6 * size_t(px))};
         const float* fi = fg_in;
         const float* bi = bg_in;
@@ -674,12 +714,17 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
             J1.h = h;
             J1.nb = sweep_bands(h, ps[pi]);
             J1.band_base = 0;
-            ck(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * size_t(J1.nb + 1), s), "memset");
+            J1.vec4 = vec4_ok(J1);
+            ck(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * size_t(3 * J1.nb + 1), s), "memset");
             SweepJob* d = A.take<SweepJob>(1);
             ck(cudaMemcpyAsync(d, &J1, sizeof(J1), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
+            const std::vector<int2> ord = band_order({J1});
+            int2* dord = A.take<int2>(ord.size());
+            ck(cudaMemcpyAsync(dord, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice, s),
+               "cudaMemcpyAsync(order)");
             {
                 ProfScope pr(s, 0, 64.0 * double(px));
-                ck(launch_sweep(ps[pi], d, 1, J1.nb, ctr, float(regularization), float(gradient_weight), s),
+                ck(launch_sweep(ps[pi], d, dord, 3 * J1.nb, ctr, float(regularization), float(gradient_weight), s),
                    "sweep_kernel");
             }
             fi = J1.fg_out;

@@ -66,3 +66,35 @@ for cfg in [synth.C1, synth.C2, synth.C3]:
         torch.cuda.synchronize()
     st = fgm.profile.stats()
     print(f"{cfg.name}: {ms:.3f} ms/solve  {cfg.width * cfg.height / ms / 1e3:.1f} MP/s  {st}", flush=True)
+
+# 4) batch (config 4)
+t0 = time.time()
+batch = synth.make_batch(device="cuda")
+torch.cuda.synchronize()
+print(f"batch generated in {time.time()-t0:.1f}s, {sum(x[0].shape[1]*x[0].shape[2] for x in batch)/1e6:.1f} MP", flush=True)
+imgs = [b[0] for b in batch]
+alps = [b[1] for b in batch]
+outs = fgm.batch_solve_cuda(imgs, alps, P)
+for _ in range(2):
+    fgm.batch_solve_cuda(imgs, alps, P, outputs=outs)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(3):
+    fgm.batch_solve_cuda(imgs, alps, P, outputs=outs)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 3
+mp = sum(x.shape[1] * x.shape[2] for x in imgs) / 1e6
+with fgm.profile():
+    fgm.batch_solve_cuda(imgs, alps, P, outputs=outs)
+    torch.cuda.synchronize()
+st = fgm.profile.stats()
+sw = st["sweep"]
+print(f"c4 batch: {ms:.2f} ms  {mp / ms * 1e3:.0f} MP/s  sweep {sw['ms']:.2f} ms {sw['alg_bytes']/sw['ms']/1e6:.0f} GB/s  {st}", flush=True)
+# spot-check parity of a few batch members
+for i in [0, 1, 2]:
+    of, ob = O.ml_solve(imgs[i].double().cpu().numpy(), alps[i].double().cpu().numpy(), OP)
+    print(f"batch[{i}] {tuple(imgs[i].shape)}")
+    cmp("fg", outs[i][0].cpu().double().numpy(), of)
+    cmp("bg", outs[i][1].cpu().double().numpy(), ob)
