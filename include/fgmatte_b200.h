@@ -83,6 +83,15 @@ int fgm_ml_solve_levels_f32(const float* image, const float* alpha, int w, int h
 int fgm_batch_solve_f32(int n_images, const float* const* images, const float* const* alphas, const int* widths,
                         const int* heights, const fgm_params* p, float* const* fgs, float* const* bgs, void* stream);
 
+/* The same batch from HOST buffers (pinned for full PCIe speed): the images
+ * are split into sub-batches whose host->device copies, solve and
+ * device->host copies overlap on separate streams (two sub-batches of device
+ * workspace in flight).  Synchronous.
+ * The reference has no batch entry point; this is the end-to-end path the
+ * benchmark's e2e figure is measured through. */
+int fgm_batch_solve_host_f32(int n_images, const float* const* images, const float* const* alphas, const int* widths,
+                             const int* heights, const fgm_params* p, float* const* fgs, float* const* bgs);
+
 /* Bilinear, centre-aligned, edge-clamped resize of `nplanes` planes with
  * clamp01, identity copy at equal size (image.cpp:71-133).  Device pointers. */
 int fgm_resize_f32(const float* src, int sw, int sh, int nplanes, float* dst, int dw, int dh, void* stream);

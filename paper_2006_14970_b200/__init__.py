@@ -29,6 +29,7 @@ __all__ = [
     "ml_foreground_background_cuda",
     "ml_foreground_background_levels_cuda",
     "batch_solve_cuda",
+    "batch_solve_host",
     "resize",
     "resize_cuda",
     "sweep_passes_cuda",
@@ -99,6 +100,8 @@ def _load():
                                           C.c_int, vp]
     L.fgm_batch_solve_f32.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(vp), ip, ip, P, C.POINTER(vp),
                                       C.POINTER(vp), vp]
+    L.fgm_batch_solve_host_f32.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(vp), ip, ip, P, C.POINTER(vp),
+                                           C.POINTER(vp)]
     L.fgm_resize_f32.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp]
     L.fgm_sweep_passes_f32.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp, vp,
                                        vp]
@@ -284,6 +287,34 @@ def batch_solve_cuda(images: Sequence, alphas: Sequence, params: Params = Params
     _check(_load().fgm_batch_solve_f32(n, V(*[x.data_ptr() for x in imgs]), V(*[a.data_ptr() for a in alps]), ws,
                                        hs, C.byref(p), V(*[o[0].data_ptr() for o in outputs]),
                                        V(*[o[1].data_ptr() for o in outputs]), _stream_ptr(imgs[0].device)))
+    return outputs
+
+
+def batch_solve_host(images: Sequence, alphas: Sequence, params: Params = Params(), outputs=None):
+    """Batch solve from HOST float32 tensors/arrays (pin them for full PCIe
+    speed): copies in, solves on the GPU and copies out, overlapped across
+    sub-batches.  `outputs` may pass preallocated host [(fg, bg), ...]."""
+    import torch
+
+    n = len(images)
+    imgs = [torch.as_tensor(x) for x in images]
+    alps = [torch.as_tensor(x) for x in alphas]
+    for x, a in zip(imgs, alps):
+        if x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous() or x.dim() != 3 or x.shape[0] != 3:
+            raise TypeError("batch_solve_host: images must be contiguous host float32 (3, H, W)")
+        if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous() or tuple(a.shape) != tuple(x.shape[1:]):
+            raise TypeError("batch_solve_host: alphas must be contiguous host float32 (H, W)")
+    if outputs is None:
+        outputs = [(torch.empty_like(x), torch.empty_like(x)) for x in imgs]
+    if n == 0:
+        return outputs
+    V = C.c_void_p * n
+    ws = (C.c_int * n)(*[x.shape[2] for x in imgs])
+    hs = (C.c_int * n)(*[x.shape[1] for x in imgs])
+    p = params.c()
+    _check(_load().fgm_batch_solve_host_f32(n, V(*[x.data_ptr() for x in imgs]), V(*[a.data_ptr() for a in alps]),
+                                            ws, hs, C.byref(p), V(*[o[0].data_ptr() for o in outputs]),
+                                            V(*[o[1].data_ptr() for o in outputs])))
     return outputs
 
 

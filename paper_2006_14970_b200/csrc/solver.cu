@@ -277,6 +277,42 @@ void carve(Plan& P, Arena& A) {
     P.stream = A.take<float>(P.stream_floats);
 }
 
+// Pinned staging for job-descriptor uploads: a small per-thread ring, each
+// slot reused only after its previous copy completed (an H2D copy from
+// pageable memory may synchronise with the stream, which would serialise the
+// overlapped host-buffer batch path).
+struct PinnedSlot {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+};
+struct PinnedRing {
+    PinnedSlot slot[4];
+    int next = 0;
+    ~PinnedRing() {
+        for (auto& s : slot) {
+            if (s.ev) cudaEventDestroy(s.ev);
+            if (s.p) cudaFreeHost(s.p);
+        }
+    }
+    void* stage(const void* src, size_t bytes, cudaStream_t s, void* dst) {
+        PinnedSlot& sl = slot[next];
+        next = (next + 1) % 4;
+        if (sl.ev) ck(cudaEventSynchronize(sl.ev), "cudaEventSynchronize");
+        else ck(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming), "cudaEventCreate");
+        if (sl.cap < bytes) {
+            if (sl.p) cudaFreeHost(sl.p);
+            sl.cap = std::max<size_t>(bytes, 1 << 16);
+            ck(cudaHostAlloc(&sl.p, sl.cap, cudaHostAllocDefault), "cudaHostAlloc");
+        }
+        std::memcpy(sl.p, src, bytes);
+        ck(cudaMemcpyAsync(dst, sl.p, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
+        ck(cudaEventRecord(sl.ev, s), "cudaEventRecord");
+        return dst;
+    }
+};
+thread_local PinnedRing g_pinned;
+
 // Host-side staging of every job descriptor of one solve: one H2D copy and
 // one memset of the dependency counters per solve.
 struct JobStage {
@@ -482,7 +518,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
         sjp->progress = dctr + reinterpret_cast<uintptr_t>(sjp->progress);
     }
     ck(cudaMemsetAsync(dctr, 0, std::max<size_t>(st.counters, 1) * sizeof(unsigned), s), "cudaMemsetAsync");
-    ck(cudaMemcpyAsync(djobs, st.host.data(), st.host.size(), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
+    g_pinned.stage(st.host.data(), st.host.size(), s, djobs);
 
     for (const LaunchRec& r : launches) {
         switch (r.kind) {
@@ -641,6 +677,101 @@ static int host_solve_impl(const void* image, const void* alpha, int w, int h, c
             ck(cudaMemcpyAsync(bg, dout + 3 * n, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, s), "D2H");
         }
         ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    });
+}
+
+int fgm_batch_solve_host_f32(int n_images, const float* const* images, const float* const* alphas, const int* widths,
+                             const int* heights, const fgm_params* p, float* const* fgs, float* const* bgs) {
+    return guarded([&] {
+        if (n_images < 0) throw InvalidArgument("fgm_batch_solve_host_f32: n_images < 0");
+        validate(p);
+        for (int i = 0; i < n_images; ++i) check_dims(widths[i], heights[i]);
+        if (n_images == 0) return;
+        require_device();
+        // Sub-batches of ~1/8 of the pixels (at least one image each): copy-in
+        // of group g+1 and copy-out of group g-1 overlap the solve of group g.
+        size_t total = 0;
+        for (int i = 0; i < n_images; ++i) total += size_t(widths[i]) * heights[i];
+        const size_t target = std::max<size_t>(total / 8, 1);
+        std::vector<std::pair<int, int>> groups;  // [begin, end)
+        for (int b = 0; b < n_images;) {
+            int e = b;
+            size_t px = 0;
+            while (e < n_images && (e == b || px < target)) px += size_t(widths[e]) * heights[e], ++e;
+            groups.push_back({b, e});
+            b = e;
+        }
+        cudaStream_t sc, sin, sout;
+        ck(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking), "cudaStreamCreate");
+        struct SG {
+            cudaStream_t a, b, c;
+            ~SG() {
+                cudaStreamSynchronize(a);
+                cudaStreamSynchronize(b);
+                cudaStreamSynchronize(c);
+                cudaStreamDestroy(a);
+                cudaStreamDestroy(b);
+                cudaStreamDestroy(c);
+            }
+        } sg{sc, sin, sout};
+        // two device slots of the largest group, 10 floats per pixel each
+        size_t gmax = 0;
+        for (auto [b, e] : groups) {
+            size_t px = 0;
+            for (int i = b; i < e; ++i) px += size_t(widths[i]) * heights[i];
+            gmax = std::max(gmax, px);
+        }
+        const size_t slot_floats = 10 * gmax + 64 * size_t(n_images);
+        float* dbuf = nullptr;
+        ck(cudaMallocAsync(reinterpret_cast<void**>(&dbuf), 2 * slot_floats * sizeof(float), sc), "cudaMallocAsync");
+        std::vector<cudaEvent_t> ev_in(groups.size()), ev_done(groups.size()), ev_out(groups.size());
+        for (size_t g = 0; g < groups.size(); ++g) {
+            ck(cudaEventCreateWithFlags(&ev_in[g], cudaEventDisableTiming), "cudaEventCreate");
+            ck(cudaEventCreateWithFlags(&ev_done[g], cudaEventDisableTiming), "cudaEventCreate");
+            ck(cudaEventCreateWithFlags(&ev_out[g], cudaEventDisableTiming), "cudaEventCreate");
+        }
+        ck(cudaStreamSynchronize(sc), "cudaStreamSynchronize");
+        for (size_t g = 0; g < groups.size(); ++g) {
+            const auto [b, e] = groups[g];
+            float* slot = dbuf + (g & 1) * slot_floats;
+            // the slot's previous user (group g-2) must have been copied out
+            if (g >= 2) ck(cudaStreamWaitEvent(sin, ev_out[g - 2], 0), "cudaStreamWaitEvent");
+            std::vector<ImageIO> io;
+            size_t off = 0;
+            for (int i = b; i < e; ++i) {
+                const size_t n = size_t(widths[i]) * heights[i];
+                float* di = slot + off;
+                float* da = di + 3 * n;
+                float* dfg = da + n;
+                float* dbg = dfg + 3 * n;
+                off += (10 * n + 63) / 64 * 64;
+                ck(cudaMemcpyAsync(di, images[i], 3 * n * sizeof(float), cudaMemcpyHostToDevice, sin), "H2D");
+                ck(cudaMemcpyAsync(da, alphas[i], n * sizeof(float), cudaMemcpyHostToDevice, sin), "H2D");
+                io.push_back({di, da, widths[i], heights[i], dfg, dbg, nullptr, nullptr});
+            }
+            ck(cudaEventRecord(ev_in[g], sin), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(sc, ev_in[g], 0), "cudaStreamWaitEvent");
+            solve_batch(io, p, sc);
+            ck(cudaEventRecord(ev_done[g], sc), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(sout, ev_done[g], 0), "cudaStreamWaitEvent");
+            for (int i = b; i < e; ++i) {
+                const ImageIO& x = io[size_t(i - b)];
+                const size_t n = size_t(widths[i]) * heights[i];
+                ck(cudaMemcpyAsync(fgs[i], x.fg, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, sout), "D2H");
+                ck(cudaMemcpyAsync(bgs[i], x.bg, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, sout), "D2H");
+            }
+            ck(cudaEventRecord(ev_out[g], sout), "cudaEventRecord");
+        }
+        ck(cudaStreamSynchronize(sout), "cudaStreamSynchronize");
+        ck(cudaFreeAsync(dbuf, sc), "cudaFreeAsync");
+        ck(cudaStreamSynchronize(sc), "cudaStreamSynchronize");
+        for (size_t g = 0; g < groups.size(); ++g) {
+            cudaEventDestroy(ev_in[g]);
+            cudaEventDestroy(ev_done[g]);
+            cudaEventDestroy(ev_out[g]);
+        }
     });
 }
 

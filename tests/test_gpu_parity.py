@@ -1,0 +1,275 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the fp64 oracle,
+the reference's golden fixtures and the reference's own property tests.
+
+Tolerance (fp32 vs fp64, on F and B, per level and final): max-abs TOL_MAX,
+mean-abs TOL_MEAN (conftest.py).  Bitwise where the reference's tests are
+bitwise and fp32 permits it (exchange / permutation symmetry, determinism,
+constant preservation of resize)."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import TOL_MAX, TOL_MEAN, assert_close, golden_files
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x, cuda):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float32).to(cuda)
+
+
+def params_from(fgm, p):
+    return fgm.Params(omega=p.omega, eps_r=p.eps_r, low_res_threshold=p.low_res_threshold, iters_low=p.iters_low,
+                      iters_high=p.iters_high)
+
+
+def gpu_solve(fgm, cuda, img, a, p):
+    f, b = fgm.ml_foreground_background_cuda(dev(img, cuda), dev(a, cuda), params_from(fgm, p))
+    torch.cuda.synchronize()
+    return f.double().cpu().numpy(), b.double().cpu().numpy()
+
+
+# ---- golden fixtures generated from the unmodified reference ---------------
+@pytest.mark.parametrize("path", golden_files(), ids=lambda p: p.rsplit("/", 1)[-1])
+def test_golden_fixtures(fgm, cuda, oracle_mod, path):
+    z = np.load(path)
+    pr = z["params"]
+    p = oracle_mod.Params(float(pr[0]), float(pr[1]), int(pr[2]), int(pr[3]), int(pr[4]))
+    f, b = gpu_solve(fgm, cuda, z["image"], z["alpha"], p)
+    assert_close("fg", f, z["fg"])
+    assert_close("bg", b, z["bg"])
+
+
+# ---- shapes, ragged edges and parameter variants vs the fp64 oracle --------
+SHAPES = [(1, 1), (2, 1), (1, 2), (3, 3), (5, 3), (1, 40), (40, 1), (31, 24), (45, 45), (46, 46), (64, 64), (65, 33),
+          (33, 65), (97, 53), (130, 9), (9, 130), (200, 136), (333, 517), (517, 333), (512, 512)]
+
+
+@pytest.mark.parametrize("w,h", SHAPES)
+def test_ml_vs_oracle_shapes(fgm, cuda, orc, oracle_mod, w, h):
+    from paper_2006_14970_b200 import synth
+
+    img, a = synth.make_composite(w, h, 100 + w * 7 + h, 3, 2.5)
+    img, a = img.numpy(), a.numpy()
+    for p in (oracle_mod.Params(), oracle_mod.REFERENCE_DEFAULTS):
+        f, b = gpu_solve(fgm, cuda, img, a, p)
+        of, ob = orc.ml_solve(img.astype(np.float64), a.astype(np.float64), p)
+        assert_close(f"fg {w}x{h}", f, of)
+        assert_close(f"bg {w}x{h}", b, ob)
+
+
+@pytest.mark.parametrize("kw", [dict(iters_high=1), dict(iters_high=3), dict(iters_high=5), dict(iters_high=8),
+                                dict(iters_high=10), dict(low_res_threshold=8, iters_low=3),
+                                dict(low_res_threshold=100, iters_low=7), dict(omega=0.0, eps_r=0.5),
+                                dict(omega=5.0, eps_r=1e-6)])
+def test_ml_vs_oracle_params(fgm, cuda, orc, oracle_mod, kw):
+    from paper_2006_14970_b200 import synth
+
+    img, a = synth.make_composite(150, 110, 55, 3, 3.0)
+    img, a = img.numpy(), a.numpy()
+    p = oracle_mod.Params(**kw)
+    f, b = gpu_solve(fgm, cuda, img, a, p)
+    of, ob = orc.ml_solve(img.astype(np.float64), a.astype(np.float64), p)
+    assert_close("fg", f, of)
+    assert_close("bg", b, ob)
+
+
+def test_random_inputs_vs_oracle(fgm, cuda, orc, oracle_mod):
+    rng = np.random.default_rng(5)
+    for (w, h) in [(77, 41), (256, 200)]:
+        img = rng.random((3, h, w)).astype(np.float32)
+        a = rng.random((h, w)).astype(np.float32)
+        for p in (oracle_mod.Params(), oracle_mod.REFERENCE_DEFAULTS):
+            f, b = gpu_solve(fgm, cuda, img, a, p)
+            of, ob = orc.ml_solve(img.astype(np.float64), a.astype(np.float64), p)
+            assert_close("fg", f, of)
+            assert_close("bg", b, ob)
+
+
+def test_unclamped_inputs_top_level_identity(fgm, cuda, orc, oracle_mod):
+    # The C++ API does not clamp inputs; the last level resizes the original
+    # as an unclamped identity copy (image.cpp:116,127).
+    rng = np.random.default_rng(6)
+    img = (rng.random((3, 60, 90)) * 1.4 - 0.2).astype(np.float32)
+    a = rng.random((60, 90)).astype(np.float32)
+    f, b = gpu_solve(fgm, cuda, img, a, oracle_mod.Params())
+    of, ob = orc.ml_solve(img.astype(np.float64), a.astype(np.float64), oracle_mod.Params())
+    assert_close("fg", f, of)
+    assert_close("bg", b, ob)
+
+
+# ---- per-level parity ---------------------------------------------------------
+@pytest.mark.parametrize("w,h", [(300, 200), (1920, 1080)])
+def test_per_level_vs_oracle(fgm, cuda, orc, oracle_mod, w, h):
+    from paper_2006_14970_b200 import synth
+
+    img, a = synth.make_composite(w, h, 77, 5, 4.0, hair=(w == 1920))
+    p = oracle_mod.Params()
+    f, b, lf, lb = fgm.ml_foreground_background_levels_cuda(img.to(cuda), a.to(cuda), params_from(fgm, p))
+    torch.cuda.synchronize()
+    of, ob, olf, olb = orc.ml_solve(img.double().numpy(), a.double().numpy(), p, levels=True)
+    assert len(lf) == len(olf)
+    for l in range(len(lf)):
+        assert_close(f"fg level {l}", lf[l].double().cpu().numpy(), olf[l])
+        assert_close(f"bg level {l}", lb[l].double().cpu().numpy(), olb[l])
+    assert np.array_equal(lf[-1].cpu().numpy(), f.cpu().numpy())
+
+
+# ---- single level: K fused sweeps vs `iterations` oracle sweeps ---------------
+@pytest.mark.parametrize("w,h,K", [(37, 29, 1), (64, 64, 2), (100, 70, 3), (130, 97, 4), (50, 40, 8), (33, 200, 10),
+                                   (1, 50, 2), (50, 1, 2), (300, 33, 2), (257, 129, 2)])
+def test_sweep_passes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, K):
+    rng = np.random.default_rng(w * 31 + h * 7 + K)
+    img = rng.random((3, h, w)).astype(np.float32)
+    a = rng.random((h, w)).astype(np.float32)
+    f0 = rng.random((3, h, w)).astype(np.float32)
+    b0 = rng.random((3, h, w)).astype(np.float32)
+    p = oracle_mod.Params()
+    of, ob = orc.sweep(img.astype(np.float64), a.astype(np.float64), f0.astype(np.float64), b0.astype(np.float64), p,
+                       K)
+    gf, gb = fgm.sweep_passes_cuda(dev(img, cuda), dev(a, cuda), dev(f0, cuda), dev(b0, cuda), K, p.eps_r, p.omega)
+    torch.cuda.synchronize()
+    assert_close("fg", gf.double().cpu().numpy(), of, tol_max=2e-5, tol_mean=1e-6)
+    assert_close("bg", gb.double().cpu().numpy(), ob, tol_max=2e-5, tol_mean=1e-6)
+
+
+# ---- resize kernel: image.cpp:71-133, test_image.cpp:88-121 --------------------
+def test_resize_golden_row_bitwise(fgm, cuda):
+    out = fgm.resize_cuda(dev(np.array([[[0.0, 1.0]]]), cuda), 4, 1)
+    assert out[0, 0].tolist() == [0.0, 0.25, 0.75, 1.0]
+
+
+def test_resize_constants_bitwise(fgm, cuda):
+    out = fgm.resize_cuda(dev(np.full((3, 4, 5), 0.77), cuda), 13, 9)
+    assert bool((out == torch.tensor(0.77, dtype=torch.float32)).all())
+
+
+def test_resize_vs_reference_fixture(fgm, cuda):
+    z = np.load(golden_files("resize_cases.npz")[0])
+    src = dev(z["src"], cuda)
+    for key, (w, h) in [("up", (29, 17)), ("down", (4, 3)), ("mixed", (20, 5))]:
+        out = fgm.resize_cuda(src, w, h).double().cpu().numpy()
+        assert np.abs(out - z[key]).max() < 1e-6
+
+
+def test_resize_identity_and_errors(fgm, cuda):
+    x = torch.rand(3, 6, 9, device=cuda)
+    assert torch.equal(fgm.resize_cuda(x, 9, 6), x)
+    with pytest.raises(ValueError, match="resize: target size must be >= 1x1"):
+        fgm.resize_cuda(x, 0, 3)
+
+
+# ---- the reference's property tests (test_multilevel.cpp:143-301) on the GPU ----
+def test_constant_binary_alpha(fgm, cuda, oracle_mod):  # :143-158
+    img = np.stack([np.full((21, 33), 0.2 + 0.25 * c, np.float32) for c in range(3)])
+    f, _ = gpu_solve(fgm, cuda, img, np.ones((21, 33), np.float32), oracle_mod.REFERENCE_DEFAULTS)
+    assert np.abs(f - img).max() < 1e-6
+    _, b = gpu_solve(fgm, cuda, img, np.zeros((21, 33), np.float32), oracle_mod.REFERENCE_DEFAULTS)
+    assert np.abs(b - img).max() < 1e-6
+
+
+@pytest.mark.parametrize("size", [64, 256])
+def test_exchange_symmetry_bitwise(fgm, cuda, oracle_mod, size):  # :167-180
+    rng = np.random.default_rng(31)
+    img = rng.random((3, size, size)).astype(np.float32)
+    a = (rng.integers(0, 1025, (size, size)) / 1024.0).astype(np.float32)
+    for p in (oracle_mod.REFERENCE_DEFAULTS, oracle_mod.Params()):
+        f, b = gpu_solve(fgm, cuda, img, a, p)
+        fc, bc = gpu_solve(fgm, cuda, img, 1.0 - a, p)
+        assert np.array_equal(f, bc) and np.array_equal(b, fc)
+
+
+def test_channel_permutation_bitwise(fgm, cuda, oracle_mod):  # :182-197
+    rng = np.random.default_rng(37)
+    img = rng.random((3, 170, 240)).astype(np.float32)
+    a = rng.random((170, 240)).astype(np.float32)
+    perm = [2, 0, 1]
+    f, b = gpu_solve(fgm, cuda, img, a, oracle_mod.Params())
+    fp, bp = gpu_solve(fgm, cuda, img[perm], a, oracle_mod.Params())
+    assert np.array_equal(fp, f[perm]) and np.array_equal(bp, b[perm])
+
+
+def test_determinism_bitwise(fgm, cuda):  # :199-206
+    from paper_2006_14970_b200 import synth
+
+    img, a = synth.make_composite(700, 500, 41, 5, 4.0)
+    img, a = img.to(cuda), a.to(cuda)
+    r1 = fgm.ml_foreground_background_cuda(img, a, fgm.BASELINE_PARAMS)
+    r2 = fgm.ml_foreground_background_cuda(img, a, fgm.BASELINE_PARAMS)
+    assert torch.equal(r1[0], r2[0]) and torch.equal(r1[1], r2[1])
+
+
+def test_one_pixel_vs_iterated_solve_pixel(fgm, cuda, orc, oracle_mod):  # :208-237
+    p = oracle_mod.REFERENCE_DEFAULTS
+    inten = [0.62, 0.31, 0.85]
+    f, b = gpu_solve(fgm, cuda, np.array(inten, np.float32).reshape(3, 1, 1), np.full((1, 1), 0.7, np.float32), p)
+    fo, bo = np.zeros(3), np.zeros(3)
+    a = float(np.float32(0.7))
+    inten32 = [float(np.float32(v)) for v in inten]
+    for _ in range(p.iters_low):
+        fo, bo = orc.solve_pixel(a, inten32, [a] * 4, [fo] * 4, [bo] * 4)
+    assert np.abs(f[:, 0, 0] - fo).max() < 1e-6 and np.abs(b[:, 0, 0] - bo).max() < 1e-6
+    assert np.abs(a * f[:, 0, 0] + (1 - a) * b[:, 0, 0] - np.array(inten32)).max() < 8 * p.eps_r
+
+
+def test_reconstruction_and_range(fgm, cuda, oracle_mod):  # :239-261, :285-301
+    from paper_2006_14970_b200 import synth
+
+    for s in range(3):
+        img, a = synth.make_composite(48, 40, 43 + s, 2, 3.0)
+        f, b = gpu_solve(fgm, cuda, img.numpy(), a.numpy(), oracle_mod.REFERENCE_DEFAULTS)
+        an = a.numpy().astype(np.float64)
+        rec = an * f + (1 - an) * b
+        m = (an > 0) & (an < 1)
+        err = (an * ((rec - img.numpy()) ** 2).sum(0))[m].sum() / m.sum()
+        assert err < 1e-3
+        assert f.min() >= 0 and f.max() <= 1 and b.min() >= 0 and b.max() <= 1
+
+
+def test_two_color_ramp(fgm, cuda, oracle_mod):  # :263-283
+    size = 64
+    ramp = np.tile(np.arange(size, dtype=np.float64) / (size - 1), (size, 1))
+    ftc, btc = np.array([0.9, 0.1, 0.1]), np.array([0.1, 0.1, 0.9])
+    img = np.clip(ramp[None] * ftc[:, None, None] + (1 - ramp[None]) * btc[:, None, None], 0, 1)
+    f, _ = gpu_solve(fgm, cuda, img.astype(np.float32), ramp.astype(np.float32), oracle_mod.REFERENCE_DEFAULTS)
+    m = ramp > 0.1
+    assert max(np.abs(f[c][m] - ftc[c]).max() for c in range(3)) < 0.02
+
+
+# ---- entry points and error behaviour ------------------------------------------
+def test_host_numpy_api_matches_oracle(fgm, orc, oracle_mod):
+    rng = np.random.default_rng(8)
+    img = rng.random((70, 90, 3))
+    a = rng.random((70, 90))
+    f, b = fgm.ml_foreground_background(img, a)  # reference defaults, HWC fp64 (bindings.cpp:146-157)
+    of, ob = orc.ml_solve(img.transpose(2, 0, 1).astype(np.float32).astype(np.float64),
+                          a.astype(np.float32).astype(np.float64), oracle_mod.REFERENCE_DEFAULTS)
+    assert f.shape == (70, 90, 3) and f.dtype == np.float64
+    assert_close("fg", f.transpose(2, 0, 1), of)
+    assert_close("bg", b.transpose(2, 0, 1), ob)
+
+
+def test_errors_on_gpu(fgm, cuda):
+    x = torch.rand(3, 8, 8, device=cuda)
+    a = torch.rand(8, 8, device=cuda)
+    with pytest.raises(ValueError, match="MlParams: eps_r must be > 0"):
+        fgm.ml_foreground_background_cuda(x, a, fgm.Params(eps_r=0.0))
+    with pytest.raises(ValueError, match="does not match image size"):
+        fgm.ml_foreground_background_cuda(x, torch.rand(8, 7, device=cuda))
+    with pytest.raises(TypeError):
+        fgm.ml_foreground_background_cuda(x.double(), a)
+
+
+def test_batch_equals_single_bitwise(fgm, cuda):
+    from paper_2006_14970_b200 import synth
+
+    sizes = [(300, 200), (64, 48), (513, 257), (96, 96), (1, 1), (40, 7)]
+    imgs, alps = [], []
+    for i, (w, h) in enumerate(sizes):
+        im, al = synth.make_composite(w, h, 900 + i, 3, 3.0)
+        imgs.append(im.to(cuda))
+        alps.append(al.to(cuda))
+    outs = fgm.batch_solve_cuda(imgs, alps, fgm.BASELINE_PARAMS)
+    for im, al, (f, b) in zip(imgs, alps, outs):
+        f1, b1 = fgm.ml_foreground_background_cuda(im, al, fgm.BASELINE_PARAMS)
+        assert torch.equal(f, f1) and torch.equal(b, b1)
