@@ -33,7 +33,8 @@ struct CoarseJob {
 
 // ---- K3: big-level sweep, skewed-band wavefront ---------------------------
 constexpr int kBandRows = 32;   // one warp = 32 skewed rows
-constexpr int kChunk = 16;      // boundary-stream publication granularity (columns)
+constexpr int kChunk = 16;      // boundary-stream polling granularity (columns)
+constexpr unsigned kStreamSentinel = 0xFFFFFFFFu;  // a NaN: never a clamped output
 
 struct SweepJob {
     const float* img;    // 3 planes
@@ -42,8 +43,7 @@ struct SweepJob {
     const float* bg_in;
     float* fg_out;
     float* bg_out;
-    float* stream;       // 3 * nb streams of sweep_stream_len(w, K) floats
-    unsigned* progress;  // 3 * nb counters (zeroed before launch)
+    float* stream;       // 3 * nb streams of sweep_stream_len(w, K) floats, sentinel-filled before launch
     long long pstride;   // w*h
     int w, h, nb, band_base;
     int vec4;            // rows are 16-byte aligned (w % 4 == 0, aligned bases): 16-byte cp.async
@@ -66,6 +66,8 @@ cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float
 // order_dev[t] = (job, 3 * band + channel) of ticket t, band-major across jobs.
 cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands, unsigned* ticket,
                          float eps, float omega, cudaStream_t s);
+// Fill every job's boundary streams with kStreamSentinel (before its sweep).
+cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, size_t max_floats, cudaStream_t s);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);
 cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s);
 size_t coarse_smem_bytes();

@@ -19,29 +19,66 @@ namespace fgm {
 // K1/K2: resample.  One CTA row-loop per destination row, threads along x
 // (coalesced stores).  Equal sizes are an unclamped copy (image.cpp:116,127).
 // ============================================================================
-__global__ void __launch_bounds__(256) resample_kernel(const ResampleJob* __restrict__ jobs) {
-    const ResampleJob J = jobs[blockIdx.y];
+template <int NP>
+__device__ __forceinline__ void resample_rows(const ResampleJob& J) {
     const bool ident = (J.sw == J.dw && J.sh == J.dh);
     for (int y = blockIdx.x; y < J.dh; y += gridDim.x) {
         if (ident) {
             for (int x = threadIdx.x; x < J.dw; x += blockDim.x) {
                 const long long i = (long long)y * J.dw + x;
-                for (int p = 0; p < J.nplanes; ++p) J.dst[p * J.dpstride + i] = J.src[p * J.spstride + i];
+                float v[NP];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) v[p] = __ldg(J.src + p * J.spstride + i);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) J.dst[p * J.dpstride + i] = v[p];
             }
             continue;
         }
         const Tap ty = make_tap_s(y, J.sh, J.sy);
+        const long long r0 = (long long)ty.i0 * J.sw, r1 = (long long)ty.i1 * J.sw;
         for (int x = threadIdx.x; x < J.dw; x += blockDim.x) {
             const Tap tx = make_tap_s(x, J.sw, J.sx);
-            const long long r0 = (long long)ty.i0 * J.sw, r1 = (long long)ty.i1 * J.sw;
             const long long o = (long long)y * J.dw + x;
-            for (int p = 0; p < J.nplanes; ++p) {
+            float a[NP], b[NP], c[NP], d[NP];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {  // all loads first (memory-level parallelism)
                 const float* s = J.src + p * J.spstride;
-                J.dst[p * J.dpstride + o] =
-                    bilerp(__ldg(s + r0 + tx.i0), __ldg(s + r0 + tx.i1), __ldg(s + r1 + tx.i0), __ldg(s + r1 + tx.i1),
-                           tx.t, ty.t);
+                a[p] = __ldg(s + r0 + tx.i0);
+                b[p] = __ldg(s + r0 + tx.i1);
+                c[p] = __ldg(s + r1 + tx.i0);
+                d[p] = __ldg(s + r1 + tx.i1);
             }
+#pragma unroll
+            for (int p = 0; p < NP; ++p) J.dst[p * J.dpstride + o] = bilerp(a[p], b[p], c[p], d[p], tx.t, ty.t);
         }
+    }
+}
+
+__global__ void __launch_bounds__(256) resample_kernel(const ResampleJob* __restrict__ jobs) {
+    const ResampleJob J = jobs[blockIdx.y];
+    if (blockIdx.x >= J.dh) return;
+    switch (J.nplanes) {
+        case 1: resample_rows<1>(J); break;
+        case 3: resample_rows<3>(J); break;
+        case 6: resample_rows<6>(J); break;
+        default:
+            for (int y = blockIdx.x; y < J.dh; y += gridDim.x) {  // generic (fgm_resize_f32 with other counts)
+                const Tap ty = make_tap_s(y, J.sh, J.sy);
+                for (int x = threadIdx.x; x < J.dw; x += blockDim.x) {
+                    const long long o = (long long)y * J.dw + x;
+                    if (J.sw == J.dw && J.sh == J.dh) {
+                        for (int p = 0; p < J.nplanes; ++p) J.dst[p * J.dpstride + o] = J.src[p * J.spstride + o];
+                        continue;
+                    }
+                    const Tap tx = make_tap_s(x, J.sw, J.sx);
+                    const long long r0 = (long long)ty.i0 * J.sw, r1 = (long long)ty.i1 * J.sw;
+                    for (int p = 0; p < J.nplanes; ++p) {
+                        const float* s = J.src + p * J.spstride;
+                        J.dst[p * J.dpstride + o] = bilerp(s[r0 + tx.i0], s[r0 + tx.i1], s[r1 + tx.i0],
+                                                           s[r1 + tx.i1], tx.t, ty.t);
+                    }
+                }
+            }
     }
 }
 

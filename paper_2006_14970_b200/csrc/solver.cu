@@ -317,7 +317,6 @@ thread_local PinnedRing g_pinned;
 // one memset of the dependency counters per solve.
 struct JobStage {
     std::vector<unsigned char> host;
-    std::vector<size_t> sweep_offsets;  // SweepJob records whose `progress` holds a counter index
     size_t counters = 0;
     template <class T>
     size_t push(const std::vector<T>& v) {
@@ -447,6 +446,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 std::vector<SweepJob> sj;
                 int total = 0;
                 double sbytes = 0;
+                size_t max_stream = 0;
                 const size_t ticket = st.counters++;
                 for (auto& a : act) {
                     Plan& P = *a.P;
@@ -478,9 +478,8 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                     J1.nb = sweep_bands(L.h, K);
                     J1.band_base = total;
                     J1.vec4 = vec4_ok(J1);
-                    J1.progress = reinterpret_cast<unsigned*>(uintptr_t(st.counters));  // patched below
-                    st.counters += 3 * size_t(J1.nb);
                     total += 3 * J1.nb;
+                    max_stream = std::max(max_stream, sweep_stream_floats(L.w, L.h, K));
                     sbytes += 64.0 * double(px);
                     sj.push_back(J1);
                 }
@@ -489,9 +488,8 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                     continue;
                 }
                 const size_t off = st.push(sj);
-                for (size_t k = 0; k < sj.size(); ++k) st.sweep_offsets.push_back(off + k * sizeof(SweepJob));
                 const size_t ooff = st.push(band_order(sj));
-                launches.push_back({kSweep, K, int(sj.size()), total, off, ticket, ooff, 0, sbytes});
+                launches.push_back({kSweep, K, int(sj.size()), total, off, ticket, ooff, (long long)max_stream, sbytes});
             }
         }
         for (auto& a : act) {  // per-level dumps (debug API)
@@ -513,10 +511,6 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
     B.reserve(al(st.host.size()) + al(std::max<size_t>(st.counters, 1) * sizeof(unsigned)), s);
     unsigned char* djobs = B.take<unsigned char>(st.host.size());
     unsigned* dctr = B.take<unsigned>(std::max<size_t>(st.counters, 1));
-    for (size_t off : st.sweep_offsets) {
-        SweepJob* sjp = reinterpret_cast<SweepJob*>(st.host.data() + off);
-        sjp->progress = dctr + reinterpret_cast<uintptr_t>(sjp->progress);
-    }
     ck(cudaMemsetAsync(dctr, 0, std::max<size_t>(st.counters, 1) * sizeof(unsigned), s), "cudaMemsetAsync");
     g_pinned.stage(st.host.data(), st.host.size(), s, djobs);
 
@@ -535,6 +529,9 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 break;
             }
             case kSweep: {
+                ck(launch_stream_fill(reinterpret_cast<const SweepJob*>(djobs + r.job_off), r.njobs, r.K,
+                                      size_t(r.max_rows), s),
+                   "stream_fill_kernel");
                 ProfScope ps(s, 0, r.bytes);
                 ck(launch_sweep(r.K, reinterpret_cast<const SweepJob*>(djobs + r.job_off),
                                 reinterpret_cast<const int2*>(djobs + r.order_off), r.total_bands, dctr + r.ticket, eps,
@@ -839,20 +836,20 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
             J1.fg_out = last ? fg_out : tmp[pi & 1];
             J1.bg_out = last ? bg_out : tmp[pi & 1] + 3 * px;
             J1.stream = stream_buf;
-            J1.progress = ctr + 1;
             J1.pstride = px;
             J1.w = w;
             J1.h = h;
             J1.nb = sweep_bands(h, ps[pi]);
             J1.band_base = 0;
             J1.vec4 = vec4_ok(J1);
-            ck(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * size_t(3 * J1.nb + 1), s), "memset");
+            ck(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s), "memset");
             SweepJob* d = A.take<SweepJob>(1);
             ck(cudaMemcpyAsync(d, &J1, sizeof(J1), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
             const std::vector<int2> ord = band_order({J1});
             int2* dord = A.take<int2>(ord.size());
             ck(cudaMemcpyAsync(dord, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice, s),
                "cudaMemcpyAsync(order)");
+            ck(launch_stream_fill(d, 1, ps[pi], sweep_stream_floats(w, h, ps[pi]), s), "stream_fill_kernel");
             {
                 ProfScope pr(s, 0, 64.0 * double(px));
                 ck(launch_sweep(ps[pi], d, dord, 3 * J1.nb, ctr, float(regularization), float(gradient_weight), s),

@@ -11,27 +11,31 @@
 //     lane updates, for every k < K, pixel (t - v - k, v - k);
 //   * every neighbour value comes from the lane itself or from lane-1 one
 //     step earlier (registers + shfl.up), except lane 0, which reads the band
-//     above's last lane from that band's boundary stream in global memory
-//     (release/acquire counters every kChunk columns, prefetched one chunk
-//     ahead when the band above is far enough ahead);
+//     above's last lane from that band's boundary stream in global memory;
 //   * bands depend only on the band above, and are handed out by an atomic
 //     ticket in dependency order (band-major across the images of a launch),
 //     so every awaited band is already resident.
 //
+// Boundary streams carry no flags: the buffer is filled with a NaN sentinel
+// before the launch, lane 31 of band q stores its K (F_c, B_c) pairs per
+// column, and band q+1 polls each 16-column chunk until no word is the
+// sentinel (outputs are clamped to [0, 1], never NaN).  Each word validates
+// itself, so no fences are needed on either side; the next chunk is fetched
+// one chunk ahead and only re-polled if it was not complete yet.
+//
 // The three colour channels share only alpha (the 2x2 matrix is common to all
 // channels, multilevel.hpp:37-43), so each (band, channel) is an independent
-// warp: it recomputes the alpha-only coefficients (pixel_coef) and runs the
-// F_c / B_c recurrence (pixel_apply) of its channel.  This triples the warps
-// per image, cuts a warp's step to ~1/3, and keeps its shared memory at ~22 KB
-// (about 10 warps per SM).
+// warp: it recomputes the alpha-only coefficients (pixel_coef1) and runs the
+// F_c / B_c recurrence (pixel_apply1) of its channel.
 //
 // Memory: each warp streams its band's rows of alpha, I_c and the initial F_c,
-// B_c through per-row shared-memory rings of 32 columns, filled by 16-byte
-// cp.async kLead columns ahead of use; element (row r, column x) sits at ring
-// column x mod 32, so the diagonal reads of a step hit 32 distinct banks and
-// every ring row of a lane is a compile-time offset from its alpha row.
-// Outputs go through a 16-column ring per row and leave as coalesced 64-byte
-// row segments (two rows per step) once complete.
+// B_c through per-row shared-memory rings of 32 columns, filled by cp.async
+// kLead columns ahead of use; element (row r, column x) sits at ring column
+// x mod 32, so the diagonal reads of a step hit 32 distinct banks and every
+// ring row of a lane is a compile-time offset from its alpha row.  Outputs go
+// through a 16-column ring per row and leave as coalesced 64-byte row segments
+// (two rows per step) once complete.  Steps run in groups of four: loads,
+// stream chunks and the border/fast decision are handled once per group.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -53,12 +57,23 @@ template <int N>
 __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ float4 ld_relaxed_v4(const float* p) {
+    float4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
     return v;
 }
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void st_relaxed_v4(float* p, float4 v) {
+    asm volatile("st.relaxed.gpu.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v2(float* p, float2 v) {
+    asm volatile("st.relaxed.gpu.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ bool is_sentinel(float v) { return __float_as_uint(v) == kStreamSentinel; }
 
 // Shared-memory geometry of one (band, channel) warp, in floats.  Alpha row r
 // (relative to the band) sits at OFF_A + (r + K) * 32; image row r at
@@ -77,14 +92,15 @@ struct Geom {
     static constexpr int OFF_O = OFF_B + NF * 32;  // [plane F/B][lane][OW]
     static constexpr int OFF_C = OFF_O + 2 * 32 * OW;
     static constexpr int CH = kChunk * K * 2;  // one boundary-stream chunk: [u][k][F,B]
-    static constexpr int TOTAL = OFF_C + 2 * CH;
+    static constexpr int CH4 = CH / 4;         // float4 per chunk (<= 32: one per lane)
+    static constexpr int TOTAL = OFF_C + CH;
     static constexpr int dI = OFF_I - OFF_A - 32;      // image row r - alpha row r
     static constexpr int dF = OFF_F - OFF_A - 32 * K;  // F row r - alpha row r
     static constexpr int dB = OFF_B - OFF_A - 32 * K;  // B row r - alpha row r
     // live alpha/image window is [t-2K+2, t+2] in row-time, plus the lead
     static_assert(kLead + 2 * K + 6 <= 32, "ring too small for the prefetch lead");
     static_assert(kLead % 4 == 0, "lead must be whole 16-byte blocks");
-    static_assert(CH % 4 == 0, "chunks are moved as float4");
+    static_assert(CH % 4 == 0 && CH4 <= 32, "a chunk is at most one float4 per lane");
 };
 
 // The global rows a lane streams into its rings (its own row and, for some
@@ -117,8 +133,8 @@ __device__ __forceinline__ RowSrc make_rowsrc(const SweepJob& J, int ch, int y0,
 }
 
 // cp.async of block b (columns 4b..4b+3) of one row into its rings.
-template <int K>
-__device__ __forceinline__ void row_block(const RowSrc& rs, int b, int w, bool vec4) {
+template <int K, bool V4>
+__device__ __forceinline__ void row_block(const RowSrc& rs, int b, int w) {
     using G = Geom<K>;
     const int x0 = 4 * b;
     if (x0 < 0 || x0 >= w) return;
@@ -127,7 +143,7 @@ __device__ __forceinline__ void row_block(const RowSrc& rs, int b, int w, bool v
     auto put = [&](unsigned s, const float* row) {
         if (!row) return;
         const float* g = row + x0;
-        if (vec4) {
+        if (V4) {
             cp_async16(s, g, nb);
         } else {
 #pragma unroll
@@ -165,16 +181,28 @@ struct LaneState {
     Coef1 co[K];      // coefficients of this step's pixels (computed one step ahead)
 };
 
+struct StepCtx {
+    const float* sm;
+    float* smw;
+    int lane, y0, w, h;
+    bool has_up, has_down;
+    int Umax;
+    float* my_stream;  // this band's stream (column 0)
+    float* FO;
+    float* BO;
+    float eps, omega;
+};
+
 // One wavefront step.  G: a pixel of this step or the next may be on the
 // image border (clamped neighbours) or an output row segment may be partial.
 template <int K, bool G>
-__device__ __forceinline__ void band_step(LaneState<K>& st, const float* sm, float* smw, int lane, int tr, int c0,
-                                          int y0, int w, int h, bool from_up, const float* chunk_now,
-                                          float* my_stream, bool stream_out, float* FO, float* BO, float eps,
-                                          float omega) {
+__device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, int tr) {
     using Gm = Geom<K>;
     constexpr int OW = Gm::OW;
+    const int lane = x_.lane, y0 = x_.y0, w = x_.w, h = x_.h;
+    const float* sm = x_.sm;
     const int aRow = Gm::OFF_A + (lane + K) * 32;
+    const int c0 = (tr - lane) & 31;
 
     float2 recv[K];
 #pragma unroll
@@ -182,9 +210,10 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const float* sm, flo
         recv[k].x = __shfl_up_sync(kFull, st.outp[k].x, 1);
         recv[k].y = __shfl_up_sync(kFull, st.outp[k].y, 1);
     }
-    if (lane == 0 && from_up) {
+    if (lane == 0 && x_.has_up && (!G || (tr >= 0 && tr < x_.Umax))) {
+        const float* cn = sm + Gm::OFF_C + (tr % kChunk) * K * 2;
 #pragma unroll
-        for (int k = 0; k < K; ++k) recv[k] = *reinterpret_cast<const float2*>(chunk_now + 2 * k);
+        for (int k = 0; k < K; ++k) recv[k] = *reinterpret_cast<const float2*>(cn + 2 * k);
     }
 
     float2 nv[K];
@@ -215,7 +244,8 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const float* sm, flo
     // coefficients of the next step's pixels (alpha/image rings only)
 #pragma unroll
     for (int k = 0; k < K; ++k)
-        st.co[k] = slot_coef<K, G>(sm, aRow, (c0 + 1 - k) & 31, k, xs0 + 1 - k, y0 + lane - k, w, h, eps, omega);
+        st.co[k] = slot_coef<K, G>(sm, aRow, (c0 + 1 - k) & 31, k, xs0 + 1 - k, y0 + lane - k, w, h, x_.eps,
+                                   x_.omega);
 
     // output ring (last sweep only)
     {
@@ -223,21 +253,22 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const float* sm, flo
         bool ok = true;
         if (G) ok = x >= 0 && x < w && y0 + lane - (K - 1) >= 0 && y0 + lane - (K - 1) < h;
         if (ok) {
-            float* o = smw + Gm::OFF_O + lane * OW + (x & (OW - 1));
+            float* o = x_.smw + Gm::OFF_O + lane * OW + (x & (OW - 1));
             o[0] = nv[K - 1].x;
             o[32 * OW] = nv[K - 1].y;
         }
     }
 
     // boundary stream for the band below: lane 31's K outputs of this step
-    if (stream_out && lane == kBandRows - 1) {
+    if (x_.has_down && lane == kBandRows - 1 && (!G || (tr - 31 >= 0 && tr - 31 < x_.Umax))) {
+        float* dst = x_.my_stream + size_t(tr - 31) * K * 2;
         if (K % 2 == 0) {  // 16-byte aligned: u * 2K floats with K even
 #pragma unroll
             for (int k = 0; k + 1 < K; k += 2)
-                *reinterpret_cast<float4*>(my_stream + 2 * k) = make_float4(nv[k].x, nv[k].y, nv[k + 1].x, nv[k + 1].y);
+                st_relaxed_v4(dst + 2 * k, make_float4(nv[k].x, nv[k].y, nv[k + 1].x, nv[k + 1].y));
         } else {
 #pragma unroll
-            for (int k = 0; k < K; ++k) *reinterpret_cast<float2*>(my_stream + 2 * k) = nv[k];
+            for (int k = 0; k < K; ++k) st_relaxed_v2(dst + 2 * k, nv[k]);
         }
     }
 
@@ -254,8 +285,8 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const float* sm, flo
         if (ok) {
             const long long off = (long long)yf * w + (xf - (OW - 1)) + col;
             const float* o = sm + Gm::OFF_O + jf * OW + col;
-            FO[off] = o[0];
-            BO[off] = o[32 * OW];
+            x_.FO[off] = o[0];
+            x_.BO[off] = o[32 * OW];
         }
         if (G && ((w - 1) & (OW - 1)) != OW - 1) {  // partial last segment of a row
             const int je = tr - (K - 1) - (w - 1);
@@ -264,8 +295,8 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const float* sm, flo
             if (je >= 0 && je < 32 && ye >= 0 && ye < h && lane < w - x0) {
                 const long long off = (long long)ye * w + x0 + lane;
                 const float* o = sm + Gm::OFF_O + je * OW + lane;
-                FO[off] = o[0];
-                BO[off] = o[32 * OW];
+                x_.FO[off] = o[0];
+                x_.BO[off] = o[32 * OW];
             }
         }
     }
@@ -277,125 +308,115 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const float* sm, flo
     }
 }
 
-// Rare path: publish `cols` finished columns of this band's stream.
-__device__ __noinline__ void publish(unsigned* p, unsigned cols) { st_release(p, cols); }
-
+// Poll chunk `u0 / kChunk` of the band above until every word of it is
+// written; leaves it in the chunk buffer.  `v` holds a load issued earlier
+// (one chunk ahead) and is re-polled only while incomplete.
 template <int K>
+__device__ __forceinline__ void acquire_chunk(float4 v, const float* up_stream, int u0, int Umax, int lane,
+                                              float* chunk) {
+    using G = Geom<K>;
+    const int nvalid = min(kChunk, Umax - u0) * K * 2;  // floats
+    const bool mine = lane < G::CH4 && 4 * lane < nvalid;
+    auto complete = [&](float4 q) {
+        if (!mine) return true;
+        const int b = 4 * lane;
+        return !(is_sentinel(q.x) || (b + 1 < nvalid && is_sentinel(q.y)) || (b + 2 < nvalid && is_sentinel(q.z)) ||
+                 (b + 3 < nvalid && is_sentinel(q.w)));
+    };
+    while (!__all_sync(kFull, complete(v))) {
+        __nanosleep(32);
+        if (mine) v = ld_relaxed_v4(up_stream + size_t(u0) * K * 2 + 4 * lane);
+    }
+    if (mine) reinterpret_cast<float4*>(chunk)[lane] = v;
+}
+
+template <int K, bool V4>
 __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int lane, float* sm, float eps,
                                          float omega) {
     using Gm = Geom<K>;
     const int w = J.w, h = J.h;
     const int y0 = q * kBandRows;
     const int Umax = w + K - 1;
-    const bool vec4 = J.vec4 != 0;
     const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sm));
     const size_t slen = sweep_stream_len(w, K);
-    const int sid = q * 3 + ch;  // stream / counter index of this (band, channel)
+    const int sid = q * 3 + ch;  // stream index of this (band, channel)
     const float* up_stream = q > 0 ? J.stream + size_t(sid - 3) * slen : nullptr;
-    float* my_stream = J.stream + size_t(sid) * slen;
-    const bool has_down = q < J.nb - 1;
-    const bool has_up = q > 0;
-    unsigned* up_prog = J.progress + (sid - 3);
-    unsigned* my_prog = J.progress + sid;
-    float* chunk = sm + Gm::OFF_C;
-    const unsigned chunk_s = sbase + 4u * Gm::OFF_C;
-    float* FO = J.fg_out + (long long)ch * J.pstride;
-    float* BO = J.bg_out + (long long)ch * J.pstride;
+
+    StepCtx cx;
+    cx.sm = sm;
+    cx.smw = sm;
+    cx.lane = lane;
+    cx.y0 = y0;
+    cx.w = w;
+    cx.h = h;
+    cx.has_up = q > 0;
+    cx.has_down = q < J.nb - 1;
+    cx.Umax = Umax;
+    cx.my_stream = J.stream + size_t(sid) * slen;
+    cx.FO = J.fg_out + (long long)ch * J.pstride;
+    cx.BO = J.bg_out + (long long)ch * J.pstride;
+    cx.eps = eps;
+    cx.omega = omega;
 
     // rows this lane streams
     const RowSrc own = make_rowsrc<K>(J, ch, y0, lane, true, true, true, sbase);
     const bool has_x = lane >= 32 - K || lane == 0;
-    const int xr = lane == 0 ? 32 : lane - 32;
-    const RowSrc ext = make_rowsrc<K>(J, ch, y0, xr, has_x, lane >= 33 - K, lane == 0, sbase);
+    const RowSrc ext = make_rowsrc<K>(J, ch, y0, lane == 0 ? 32 : lane - 32, has_x, lane >= 33 - K, lane == 0, sbase);
 
     LaneState<K> st;
 #pragma unroll
     for (int k = 0; k < K; ++k) st.outp[k] = st.rprev[k] = make_float2(0.0f, 0.0f);
 
-    // prologue: blocks below the first in-loop issue (tr = -4 loads block
+    // prologue: blocks below the first in-loop issue (t4 = -4 loads block
     // (kLead - r) / 4 of row r)
-    for (int b = 0; b < ((Gm::kLead - own.r) >> 2); ++b) row_block<K>(own, b, w, vec4);
+    for (int b = 0; b < ((Gm::kLead - own.r) >> 2); ++b) row_block<K, V4>(own, b, w);
     if (has_x)
-        for (int b = 0; b < ((Gm::kLead - ext.r) >> 2); ++b) row_block<K>(ext, b, w, vec4);
+        for (int b = 0; b < ((Gm::kLead - ext.r) >> 2); ++b) row_block<K, V4>(ext, b, w);
     cp_commit();
+    // the band above's first chunk, polled when needed
+    float4 pend = make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool lane_ch = lane < Gm::CH4;
+    if (cx.has_up && lane_ch) pend = ld_relaxed_v4(up_stream + 4 * lane);
 
-    // Border steps: bands touching row 0 or h-1, else the first and last ~32.
+    // Border groups: bands touching row 0 or h-1, else the first and last ~32
+    // steps.  Fast groups need no neighbour clamping and no bounds checks.
     const bool yband = y0 - (K - 1) <= 0 || y0 + 31 >= h - 1;
-    const int fast_lo = 32 + K, fast_hi = w - 2;  // fast steps: [fast_lo, fast_hi)
+    const int fast_lo = 32 + K, fast_hi = w - 2;  // a step tr is fast iff fast_lo <= tr < fast_hi
     const int tend = 31 + Umax;                   // lane 31's last column is Umax-1
-    bool pref = false;   // next chunk already prefetched (cp.async)
-    unsigned pnext = 0;  // progress seen by the non-blocking check
-    for (int tr = -4; tr < tend; ++tr) {
-        if ((tr & 3) == 0) {
-            row_block<K>(own, (tr + 4 + Gm::kLead - own.r) >> 2, w, vec4);
-            if (has_x) row_block<K>(ext, (tr + 4 + Gm::kLead - ext.r) >> 2, w, vec4);
-            cp_commit();
-            cp_wait<Gm::kLead / 4 - 1>();
-        }
-        if (tr == -1) cp_wait<1>();  // the prologue group
-        const bool in_up = has_up && tr >= 0 && tr < Umax;
-        if (in_up && (tr % kChunk) == 0) {
-            // chunk tr / kChunk of the band above: prefetched, or wait and load
-            if (pref) {
-                cp_wait<2>();  // the prefetch went out >= 12 steps ago
-            } else {
-                const unsigned need = unsigned(min(tr + kChunk, Umax));
-                while (ld_relaxed(up_prog) < need) __nanosleep(32);
-                fence_acq_rel();
-                const int n4 = (int(need) - tr) * K / 2;  // float4 count (K*2 floats per column)
-                const int nrem = (int(need) - tr) * K * 2 - 4 * n4;
-                const float4* src = reinterpret_cast<const float4*>(up_stream + size_t(tr) * K * 2);
-                float* dstf = chunk + ((tr / kChunk) & 1) * Gm::CH;
-                float4* dst = reinterpret_cast<float4*>(dstf);
-                for (int e = lane; e < n4; e += 32) dst[e] = __ldcg(src + e);
-                if (lane < nrem) dstf[4 * n4 + lane] = __ldcg(up_stream + size_t(tr) * K * 2 + 4 * n4 + lane);
-            }
-            pref = false;
-            if (tr + kChunk < Umax) pnext = ld_relaxed(up_prog);  // looked at 4 steps later
-        }
-        if (in_up && (tr % kChunk) == 4 && tr + kChunk - 4 < Umax) {
-            const int nxt = tr - 4 + kChunk;  // first column of the next chunk
-            const unsigned need = unsigned(min(nxt + kChunk, Umax));
-            // only whole chunks are prefetched (a short last chunk is loaded synchronously)
-            if (int(need) == nxt + kChunk && pnext >= need) {
-                fence_acq_rel();
-                const int n4 = kChunk * K / 2;
-                const float* src = up_stream + size_t(nxt) * K * 2;
-                const unsigned dst = chunk_s + 4u * unsigned(((nxt / kChunk) & 1) * Gm::CH);
-                for (int e = lane; e < n4; e += 32) cp_async16(dst + 16u * e, src + 4 * e, 16);
-                cp_commit();
-                pref = true;
-            }
-        }
-        __syncwarp();
-        if (tr < -1) continue;
-        const int c0 = (tr - lane) & 31;
-        if (tr == -1) {  // coefficients of step 0
+    for (int t4 = -4; t4 < tend; t4 += 4) {
+        row_block<K, V4>(own, (t4 + 4 + Gm::kLead - own.r) >> 2, w);
+        if (has_x) row_block<K, V4>(ext, (t4 + 4 + Gm::kLead - ext.r) >> 2, w);
+        cp_commit();
+        cp_wait<Gm::kLead / 4 - 1>();
+        if (t4 < 0) {
+            cp_wait<1>();  // the prologue group
+            __syncwarp();
             const int aRow = Gm::OFF_A + (lane + K) * 32;
 #pragma unroll
-            for (int k = 0; k < K; ++k)
-                st.co[k] = slot_coef<K, true>(sm, aRow, (c0 + 1 - k) & 31, k, -lane - k, y0 + lane - k, w, h, eps,
-                                              omega);
+            for (int k = 0; k < K; ++k)  // coefficients of step 0
+                st.co[k] = slot_coef<K, true>(sm, aRow, (-lane + 1 - k - 1) & 31, k, -lane - k, y0 + lane - k, w, h,
+                                              eps, omega);
             continue;
         }
-        const float* chunk_now = chunk + ((tr / kChunk) & 1) * Gm::CH + (tr % kChunk) * K * 2;
-        const int u31 = tr - 31;
-        const bool sout = has_down && u31 >= 0 && u31 < Umax;
-        float* sdst = my_stream + size_t(max(u31, 0)) * K * 2;
-        if (yband || tr < fast_lo || tr >= fast_hi)
-            band_step<K, true>(st, sm, sm, lane, tr, c0, y0, w, h, in_up, chunk_now, sdst, sout, FO, BO, eps, omega);
-        else
-            band_step<K, false>(st, sm, sm, lane, tr, c0, y0, w, h, in_up, chunk_now, sdst, sout, FO, BO, eps, omega);
-        if (sout && (((u31 + 1) % kChunk) == 0 || u31 + 1 == Umax)) {
-            if (lane == kBandRows - 1) publish(my_prog, unsigned(u31 + 1));
-            __syncwarp();
+        if (cx.has_up && (t4 % kChunk) == 0 && t4 < Umax) {
+            acquire_chunk<K>(pend, up_stream, t4, Umax, lane, sm + Gm::OFF_C);
+            if (t4 + kChunk < Umax && lane_ch)  // prefetch the next chunk
+                pend = ld_relaxed_v4(up_stream + size_t(t4 + kChunk) * K * 2 + 4 * lane);
+        }
+        __syncwarp();
+        if (!yband && t4 >= fast_lo && t4 + 4 <= fast_hi) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s) band_step<K, false>(st, cx, t4 + s);
+        } else {
+#pragma unroll 1
+            for (int s = 0; s < 4; ++s) band_step<K, true>(st, cx, t4 + s);
         }
     }
     cp_wait<0>();
     __syncwarp();
 }
 
-template <int K>
+template <int K, bool V4>
 __global__ void __launch_bounds__(32) sweep_kernel(const SweepJob* __restrict__ jobs, const int2* __restrict__ order,
                                                     int total_items, unsigned* ticket, float eps, float omega) {
     extern __shared__ float4 sm4[];
@@ -408,7 +429,11 @@ __global__ void __launch_bounds__(32) sweep_kernel(const SweepJob* __restrict__ 
         if (tk >= unsigned(total_items)) return;
         const int2 jb = order[tk];  // (job, band * 3 + channel)
         const SweepJob J = jobs[jb.x];
-        run_band<K>(J, jb.y / 3, jb.y % 3, lane, sm, eps, omega);
+        if (V4 && !J.vec4) {
+            run_band<K, false>(J, jb.y / 3, jb.y % 3, lane, sm, eps, omega);
+        } else {
+            run_band<K, V4>(J, jb.y / 3, jb.y % 3, lane, sm, eps, omega);
+        }
     }
 }
 
@@ -418,20 +443,37 @@ cudaError_t launch_sweep_k(const SweepJob* jobs_dev, const int2* order_dev, int 
     static int grid_cap = 0;
     const size_t smem = size_t(Geom<K>::TOTAL) * sizeof(float);
     if (grid_cap == 0) {
-        cudaError_t e = cudaFuncSetAttribute(sweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaError_t e =
+            cudaFuncSetAttribute(sweep_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<K>, 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<K, true>, 32, smem);
         grid_cap = std::max(1, sms * std::max(1, per_sm));
     }
     const int grid = std::max(1, std::min(total_items, grid_cap));
-    sweep_kernel<K><<<grid, 32, smem, s>>>(jobs_dev, order_dev, total_items, ticket, eps, omega);
+    sweep_kernel<K, true><<<grid, 32, smem, s>>>(jobs_dev, order_dev, total_items, ticket, eps, omega);
     return cudaGetLastError();
 }
 
+__global__ void stream_fill_kernel(const SweepJob* __restrict__ jobs, int K) {
+    const SweepJob J = jobs[blockIdx.y];
+    const size_t n = size_t(3) * J.nb * sweep_stream_len(J.w, K) / 4;  // float4 count
+    float4* p = reinterpret_cast<float4*>(J.stream);
+    const float s = __uint_as_float(kStreamSentinel);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        p[i] = make_float4(s, s, s, s);
+}
+
 }  // namespace
+
+cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, size_t max_floats, cudaStream_t s) {
+    if (njobs <= 0) return cudaSuccess;
+    const int gx = int(std::min<size_t>(std::max<size_t>((max_floats / 4 + 255) / 256, 1), 64));
+    stream_fill_kernel<<<dim3(gx, njobs), 256, 0, s>>>(jobs_dev, K);
+    return cudaGetLastError();
+}
 
 int sweep_supported_k(int K) { return K >= 1 && K <= 4; }
 
