@@ -13,6 +13,7 @@ struct ResampleJob {
     int sw, sh, dw, dh, nplanes;
     long long spstride, dpstride;  // plane strides in floats
     double sx, sy;                 // double(sw)/double(dw), double(sh)/double(dh) (image.cpp:73)
+    int tile_base;                 // first tile of this job in the launch's flat tile space
 };
 
 // ---- K4: coarse levels, one CTA per image, shared-memory resident ---------
@@ -61,7 +62,9 @@ inline size_t sweep_stream_floats(int w, int h, int K) {
 }
 
 // Launch helpers (kernels.cu).  `jobs_dev` are device copies of the arrays.
-cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long max_px, cudaStream_t s);
+// Tiles of 128 x 8 destination pixels; total_tiles = sum over jobs.
+int resample_tiles(int dw, int dh);
+cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s);
 cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float omega, cudaStream_t s);
 // order_dev[t] = (job, 3 * band + channel) of ticket t, band-major across jobs.
 cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands, unsigned* ticket,

@@ -19,73 +19,101 @@ namespace fgm {
 // K1/K2: resample.  One CTA row-loop per destination row, threads along x
 // (coalesced stores).  Equal sizes are an unclamped copy (image.cpp:116,127).
 // ============================================================================
+// Tiles of 128 columns x kResRows rows: each thread keeps its column's x-tap
+// (fp64, once) for all rows of the tile; the tile's y-taps are computed once
+// into shared memory; every plane's four taps are loaded before any lerp.
+constexpr int kResCols = 128;
+constexpr int kResRows = 8;
+
 template <int NP>
-__device__ __forceinline__ void resample_rows(const ResampleJob& J) {
-    const bool ident = (J.sw == J.dw && J.sh == J.dh);
-    for (int y = blockIdx.x; y < J.dh; y += gridDim.x) {
-        if (ident) {
-            for (int x = threadIdx.x; x < J.dw; x += blockDim.x) {
-                const long long i = (long long)y * J.dw + x;
-                float v[NP];
+__device__ __forceinline__ void resample_tile(const ResampleJob& J, int x, int ybase, const Tap* tys) {
+    if (x >= J.dw) return;
+    const int yend = min(kResRows, J.dh - ybase);
+    if (J.sw == J.dw && J.sh == J.dh) {  // resize to the same size: unclamped copy
+        for (int r = 0; r < yend; ++r) {
+            const long long i = (long long)(ybase + r) * J.dw + x;
+            float v[NP];
 #pragma unroll
-                for (int p = 0; p < NP; ++p) v[p] = __ldg(J.src + p * J.spstride + i);
+            for (int p = 0; p < NP; ++p) v[p] = __ldg(J.src + p * J.spstride + i);
 #pragma unroll
-                for (int p = 0; p < NP; ++p) J.dst[p * J.dpstride + i] = v[p];
-            }
-            continue;
+            for (int p = 0; p < NP; ++p) J.dst[p * J.dpstride + i] = v[p];
         }
-        const Tap ty = make_tap_s(y, J.sh, J.sy);
+        return;
+    }
+    const Tap tx = make_tap_s(x, J.sw, J.sx);
+    for (int r = 0; r < yend; ++r) {
+        const Tap ty = tys[r];
         const long long r0 = (long long)ty.i0 * J.sw, r1 = (long long)ty.i1 * J.sw;
-        for (int x = threadIdx.x; x < J.dw; x += blockDim.x) {
-            const Tap tx = make_tap_s(x, J.sw, J.sx);
-            const long long o = (long long)y * J.dw + x;
-            float a[NP], b[NP], c[NP], d[NP];
+        const long long o = (long long)(ybase + r) * J.dw + x;
+        float a[NP], b[NP], c[NP], d[NP];
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {  // all loads first (memory-level parallelism)
-                const float* s = J.src + p * J.spstride;
-                a[p] = __ldg(s + r0 + tx.i0);
-                b[p] = __ldg(s + r0 + tx.i1);
-                c[p] = __ldg(s + r1 + tx.i0);
-                d[p] = __ldg(s + r1 + tx.i1);
-            }
+        for (int p = 0; p < NP; ++p) {
+            const float* s = J.src + p * J.spstride;
+            a[p] = __ldg(s + r0 + tx.i0);
+            b[p] = __ldg(s + r0 + tx.i1);
+            c[p] = __ldg(s + r1 + tx.i0);
+            d[p] = __ldg(s + r1 + tx.i1);
+        }
 #pragma unroll
-            for (int p = 0; p < NP; ++p) J.dst[p * J.dpstride + o] = bilerp(a[p], b[p], c[p], d[p], tx.t, ty.t);
+        for (int p = 0; p < NP; ++p) J.dst[p * J.dpstride + o] = bilerp(a[p], b[p], c[p], d[p], tx.t, ty.t);
+    }
+}
+
+template <>
+__device__ __forceinline__ void resample_tile<0>(const ResampleJob& J, int x, int ybase, const Tap* tys) {
+    if (x >= J.dw) return;  // generic plane count (fgm_resize_f32)
+    const int yend = min(kResRows, J.dh - ybase);
+    const bool ident = J.sw == J.dw && J.sh == J.dh;
+    const Tap tx = make_tap_s(x, J.sw, J.sx);
+    for (int r = 0; r < yend; ++r) {
+        const long long o = (long long)(ybase + r) * J.dw + x;
+        const Tap ty = tys[r];
+        const long long r0 = (long long)ty.i0 * J.sw, r1 = (long long)ty.i1 * J.sw;
+        for (int p = 0; p < J.nplanes; ++p) {
+            const float* s = J.src + p * J.spstride;
+            J.dst[p * J.dpstride + o] =
+                ident ? s[o] : bilerp(s[r0 + tx.i0], s[r0 + tx.i1], s[r1 + tx.i0], s[r1 + tx.i1], tx.t, ty.t);
         }
     }
 }
 
-__global__ void __launch_bounds__(256) resample_kernel(const ResampleJob* __restrict__ jobs) {
-    const ResampleJob J = jobs[blockIdx.y];
-    if (blockIdx.x >= J.dh) return;
-    switch (J.nplanes) {
-        case 1: resample_rows<1>(J); break;
-        case 3: resample_rows<3>(J); break;
-        case 6: resample_rows<6>(J); break;
-        default:
-            for (int y = blockIdx.x; y < J.dh; y += gridDim.x) {  // generic (fgm_resize_f32 with other counts)
-                const Tap ty = make_tap_s(y, J.sh, J.sy);
-                for (int x = threadIdx.x; x < J.dw; x += blockDim.x) {
-                    const long long o = (long long)y * J.dw + x;
-                    if (J.sw == J.dw && J.sh == J.dh) {
-                        for (int p = 0; p < J.nplanes; ++p) J.dst[p * J.dpstride + o] = J.src[p * J.spstride + o];
-                        continue;
-                    }
-                    const Tap tx = make_tap_s(x, J.sw, J.sx);
-                    const long long r0 = (long long)ty.i0 * J.sw, r1 = (long long)ty.i1 * J.sw;
-                    for (int p = 0; p < J.nplanes; ++p) {
-                        const float* s = J.src + p * J.spstride;
-                        J.dst[p * J.dpstride + o] = bilerp(s[r0 + tx.i0], s[r0 + tx.i1], s[r1 + tx.i0],
-                                                           s[r1 + tx.i1], tx.t, ty.t);
-                    }
-                }
-            }
+// Persistent blocks walk the flat tile space of all jobs of the launch.
+__global__ void __launch_bounds__(kResCols) resample_kernel(const ResampleJob* __restrict__ jobs, int njobs,
+                                                            int total_tiles) {
+    __shared__ Tap tys[kResRows];
+    for (int gt = blockIdx.x; gt < total_tiles; gt += gridDim.x) {
+        int lo = 0, hi = njobs - 1;  // last job with tile_base <= gt
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (jobs[mid].tile_base <= gt)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        const ResampleJob& J = jobs[lo];
+        const int tile = gt - J.tile_base;
+        const int tcols = (J.dw + kResCols - 1) / kResCols;
+        const int ty = tile / tcols, tx = tile - ty * tcols;
+        const int ybase = ty * kResRows, x = tx * kResCols + threadIdx.x;
+        __syncthreads();
+        if (threadIdx.x < kResRows && ybase + threadIdx.x < J.dh)
+            tys[threadIdx.x] = make_tap_s(ybase + threadIdx.x, J.sh, J.sy);
+        __syncthreads();
+        switch (J.nplanes) {
+            case 1: resample_tile<1>(J, x, ybase, tys); break;
+            case 3: resample_tile<3>(J, x, ybase, tys); break;
+            case 6: resample_tile<6>(J, x, ybase, tys); break;
+            default: resample_tile<0>(J, x, ybase, tys); break;
+        }
     }
 }
 
-cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long max_rows, cudaStream_t s) {
-    if (njobs <= 0) return cudaSuccess;
-    const int gx = int(std::min<long long>(std::max<long long>(max_rows, 1), 2048));
-    resample_kernel<<<dim3(gx, njobs), 256, 0, s>>>(jobs_dev);
+int resample_tiles(int dw, int dh) { return ((dw + kResCols - 1) / kResCols) * ((dh + kResRows - 1) / kResRows); }
+
+cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s) {
+    if (njobs <= 0 || total_tiles <= 0) return cudaSuccess;
+    const int gx = int(std::min<long long>(total_tiles, 148 * 16));
+    resample_kernel<<<gx, kResCols, 0, s>>>(jobs_dev, njobs, int(total_tiles));
     return cudaGetLastError();
 }
 

@@ -435,9 +435,13 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             }
             rj.push_back(rjob(P.fbOut, P.fbInit, Lp.w, Lp.h, L.w, L.h, 6));
             rbytes += 4.0 * 6 * (double(px) + double(ppx));
-            max_rows = std::max<long long>(max_rows, L.h);
+
         }
         if (act.empty()) continue;
+        for (auto& r : rj) {
+            r.tile_base = int(max_rows);
+            max_rows += resample_tiles(r.dw, r.dh);
+        }
         launches.push_back({kResample, 0, int(rj.size()), 0, st.push(rj), 0, 0, max_rows, rbytes});
         size_t max_passes = 0;
         for (auto& a : act) max_passes = std::max(max_passes, passes_for(a.P->lv[size_t(a.l)].iters).size());
@@ -794,9 +798,10 @@ int fgm_resize_f32(const float* src, int sw, int sh, int nplanes, float* dst, in
         Arena A;
         A.reserve(4096, s);
         ResampleJob rj = rjob(src, dst, sw, sh, dw, dh, nplanes);
+        rj.tile_base = 0;
         ResampleJob* d = A.take<ResampleJob>(1);
         ck(cudaMemcpyAsync(d, &rj, sizeof(rj), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
-        ck(launch_resample(d, 1, dh, s), "resample_kernel");
+        ck(launch_resample(d, 1, resample_tiles(dw, dh), s), "resample_kernel");
     });
 }
 
