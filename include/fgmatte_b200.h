@@ -103,6 +103,11 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
                          int h, int iterations, double regularization, double gradient_weight, float* fg_out,
                          float* bg_out, void* stream);
 
+/* Big-level sweep kernel choice: 0 = automatic (per-channel warps while they
+ * fit on the GPU, full-channel warps for larger launches), 1 = always
+ * per-channel, 2 = always full-channel.  Both produce identical results. */
+void fgm_set_sweep_mode(int mode);
+
 /* Profiling: when enabled, every kernel launch of the solver is bracketed by
  * CUDA events on its stream; fgm_kernel_stats() synchronises on the recorded
  * events and reports, for kernel class `which` (0 = big-level sweep K3,

@@ -106,6 +106,7 @@ def _load():
     L.fgm_sweep_passes_f32.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp, vp,
                                        vp]
     L.fgm_profile_enable.argtypes = [C.c_int]
+    L.fgm_set_sweep_mode.argtypes = [C.c_int]
     L.fgm_kernel_stats.argtypes = [C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]
     _lib = L
@@ -123,6 +124,11 @@ def _check(rc: int) -> None:
 
 def device_count() -> int:
     return int(_load().fgm_device_count())
+
+
+def set_sweep_mode(mode: int) -> None:
+    """0 automatic, 1 per-(band, channel) warps, 2 full-channel warps."""
+    _load().fgm_set_sweep_mode(int(mode))
 
 
 def version() -> str:

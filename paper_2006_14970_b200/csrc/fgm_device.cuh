@@ -123,6 +123,34 @@ __device__ __forceinline__ Coef1 pixel_coef1(float a, float aL, float aR, float 
     return co;
 }
 
+// Alpha-only part shared by the three channels of a pixel: the Coef1 fields
+// without the image term; p = u0/D, q = u1/D multiply I_c per channel.  Bn is
+// -Bc, kept positive (a product, never a sign-flipped NaN: these values travel
+// through sentinel-validated streams, see sweep_full.cu).
+struct Coef3 {
+    float dL, dR, dU, dD, A, A2, Bn, p, q;
+};
+
+__device__ __forceinline__ Coef3 pixel_coef3(float a, float aL, float aR, float aU, float aD, float eps,
+                                             float omega) {
+    Coef3 co;
+    co.dL = edge_weight(a, aL, eps, omega);
+    co.dR = edge_weight(a, aR, eps, omega);
+    co.dU = edge_weight(a, aU, eps, omega);
+    co.dD = edge_weight(a, aD, eps, omega);
+    const float S = __fadd_rn(__fadd_rn(__fadd_rn(co.dL, co.dR), co.dU), co.dD);
+    const float u0 = a, u1 = __fsub_rn(1.0f, a);
+    const float u00 = __fmul_rn(u0, u0), u11 = __fmul_rn(u1, u1), u01 = __fmul_rn(u0, u1);
+    const float iS = rcp_approx(S);
+    const float iD = rcp_approx(__fadd_rn(__fadd_rn(u00, u11), S));
+    co.A = __fmul_rn(iD, __fmaf_rn(u11, iS, 1.0f));
+    co.A2 = __fmul_rn(iD, __fmaf_rn(u00, iS, 1.0f));
+    co.Bn = __fmul_rn(iD, __fmul_rn(u01, iS));
+    co.p = __fmul_rn(iD, u0);
+    co.q = __fmul_rn(iD, u1);
+    return co;
+}
+
 // (x, y) = (F_c, B_c) of the four neighbours; returns the new (F_c, B_c).
 __device__ __forceinline__ float2 pixel_apply1(const Coef1& co, float2 L, float2 R, float2 U, float2 D) {
     float SF = __fmul_rn(co.dL, L.x);

@@ -11,6 +11,7 @@ struct ResampleJob {
     const float* src;
     float* dst;
     int sw, sh, dw, dh, nplanes;
+    int spitch, dpitch;            // row strides in floats
     long long spstride, dpstride;  // plane strides in floats
     double sx, sy;                 // double(sw)/double(dw), double(sh)/double(dh) (image.cpp:73)
     int tile_base;                 // first tile of this job in the launch's flat tile space
@@ -26,8 +27,10 @@ struct CoarseJob {
     int W, H;
     int nlev;
     int lw[kMaxCoarseLevels], lh[kMaxCoarseLevels], lit[kMaxCoarseLevels];
-    float* fg_out;  // last coarse level F (3 planes, stride lw*lh)
+    float* fg_out;  // last coarse level F (3 planes)
     float* bg_out;
+    int out_pitch;         // row stride of fg_out / bg_out
+    long long out_pstride; // plane stride of fg_out / bg_out
     float* lvl_fg[kMaxCoarseLevels];  // optional per-level dumps (debug API)
     float* lvl_bg[kMaxCoarseLevels];
 };
@@ -45,17 +48,31 @@ struct SweepJob {
     float* fg_out;
     float* bg_out;
     float* stream;       // 3 * nb streams of sweep_stream_len(w, K) floats, sentinel-filled before launch
-    long long pstride;   // w*h
+    long long istride, fstride, ostride;  // plane strides: img/alpha, fg_in/bg_in, fg_out/bg_out
+    int ipitch, fpitch, opitch;           // row strides of the same
     int w, h, nb, band_base;
-    int vec4;            // rows are 16-byte aligned (w % 4 == 0, aligned bases): 16-byte cp.async
+    int vec4;            // all input rows 16-byte aligned (pitches % 4 == 0, aligned bases): 16-byte cp.async
 };
 
 // A job of one sweep launch is split into (band, channel) work items: band q,
 // channel c has stream / counter index 3q + c.  A stream holds, per skewed
 // column u, the K (F_c, B_c) pairs of the band's last row, padded to 16 bytes.
+// Row pitch of the solver's own level buffers: whole 16-byte blocks, so the
+// sweep streams them with 16-byte cp.async whatever the level width.
+inline int level_pitch(int w) { return (w + 3) & ~3; }
+
 inline int sweep_bands(int h, int K) { return (h + K - 1 + kBandRows - 1) / kBandRows; }
 __host__ __device__ inline size_t sweep_stream_len(int w, int K) {
     return (size_t(w + K - 1) * size_t(K) * 2 + 3) / 4 * 4;
+}
+// Streams of the full-channel kernel (sweep_full.cu): per column the K x 3
+// (F, B) pairs and the (K-1) passed 13-float coefficient sets, each part
+// padded to 16 bytes.
+__host__ __device__ inline size_t sweep_full_stream_len(int w, int K) {
+    return size_t(w + K - 1) * size_t((6 * K + 3) / 4 * 4 + (13 * (K - 1) + 3) / 4 * 4);
+}
+inline size_t sweep_full_stream_floats(int w, int h, int K) {
+    return size_t(sweep_bands(h, K)) * sweep_full_stream_len(w, K);
 }
 inline size_t sweep_stream_floats(int w, int h, int K) {
     return size_t(sweep_bands(h, K)) * 3 * sweep_stream_len(w, K);
@@ -69,8 +86,14 @@ cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float
 // order_dev[t] = (job, 3 * band + channel) of ticket t, band-major across jobs.
 cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands, unsigned* ticket,
                          float eps, float omega, cudaStream_t s);
-// Fill every job's boundary streams with kStreamSentinel (before its sweep).
-cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, size_t max_floats, cudaStream_t s);
+// Fill every job's boundary streams with kStreamSentinel (before its sweep);
+// full = the stream format of launch_sweep_full.
+cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, bool full, size_t max_floats,
+                               cudaStream_t s);
+// The full-channel (throughput) sweep kernel, same contract as launch_sweep;
+// order_dev holds (job, band) pairs.
+cudaError_t launch_sweep_full(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands,
+                              unsigned* ticket, float eps, float omega, cudaStream_t s);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);
 cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s);
 size_t coarse_smem_bytes();

@@ -31,20 +31,20 @@ __device__ __forceinline__ void resample_tile(const ResampleJob& J, int x, int y
     const int yend = min(kResRows, J.dh - ybase);
     if (J.sw == J.dw && J.sh == J.dh) {  // resize to the same size: unclamped copy
         for (int r = 0; r < yend; ++r) {
-            const long long i = (long long)(ybase + r) * J.dw + x;
+            const long long is = (long long)(ybase + r) * J.spitch + x, id = (long long)(ybase + r) * J.dpitch + x;
             float v[NP];
 #pragma unroll
-            for (int p = 0; p < NP; ++p) v[p] = __ldg(J.src + p * J.spstride + i);
+            for (int p = 0; p < NP; ++p) v[p] = __ldg(J.src + p * J.spstride + is);
 #pragma unroll
-            for (int p = 0; p < NP; ++p) J.dst[p * J.dpstride + i] = v[p];
+            for (int p = 0; p < NP; ++p) J.dst[p * J.dpstride + id] = v[p];
         }
         return;
     }
     const Tap tx = make_tap_s(x, J.sw, J.sx);
     for (int r = 0; r < yend; ++r) {
         const Tap ty = tys[r];
-        const long long r0 = (long long)ty.i0 * J.sw, r1 = (long long)ty.i1 * J.sw;
-        const long long o = (long long)(ybase + r) * J.dw + x;
+        const long long r0 = (long long)ty.i0 * J.spitch, r1 = (long long)ty.i1 * J.spitch;
+        const long long o = (long long)(ybase + r) * J.dpitch + x;
         float a[NP], b[NP], c[NP], d[NP];
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -66,13 +66,14 @@ __device__ __forceinline__ void resample_tile<0>(const ResampleJob& J, int x, in
     const bool ident = J.sw == J.dw && J.sh == J.dh;
     const Tap tx = make_tap_s(x, J.sw, J.sx);
     for (int r = 0; r < yend; ++r) {
-        const long long o = (long long)(ybase + r) * J.dw + x;
+        const long long o = (long long)(ybase + r) * J.dpitch + x;
+        const long long so = (long long)(ybase + r) * J.spitch + x;
         const Tap ty = tys[r];
-        const long long r0 = (long long)ty.i0 * J.sw, r1 = (long long)ty.i1 * J.sw;
+        const long long r0 = (long long)ty.i0 * J.spitch, r1 = (long long)ty.i1 * J.spitch;
         for (int p = 0; p < J.nplanes; ++p) {
             const float* s = J.src + p * J.spstride;
             J.dst[p * J.dpstride + o] =
-                ident ? s[o] : bilerp(s[r0 + tx.i0], s[r0 + tx.i1], s[r1 + tx.i0], s[r1 + tx.i1], tx.t, ty.t);
+                ident ? s[so] : bilerp(s[r0 + tx.i0], s[r0 + tx.i1], s[r1 + tx.i0], s[r1 + tx.i1], tx.t, ty.t);
         }
     }
 }
@@ -231,8 +232,10 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_kernel(const CoarseJob*
     const float* fin = sFB[(nlev - 1) & 1];
     const int n = pw * ph;
     for (int idx = threadIdx.x; idx < 3 * n; idx += blockDim.x) {
-        J.fg_out[idx] = fin[idx];
-        J.bg_out[idx] = fin[3 * n + idx];
+        const int c = idx / n, i = idx - c * n, y = i / pw, x = i - y * pw;
+        const long long o = c * J.out_pstride + (long long)y * J.out_pitch + x;
+        J.fg_out[o] = fin[idx];
+        J.bg_out[o] = fin[3 * n + idx];
     }
 }
 

@@ -121,12 +121,11 @@ __device__ __forceinline__ RowSrc make_rowsrc(const SweepJob& J, int ch, int y0,
     RowSrc rs;
     const int y = y0 + r;
     const bool ok = y >= 0 && y < J.h;
-    const long long off = (long long)y * J.w;
-    const long long po = (long long)ch * J.pstride;
-    rs.a = ok && doA ? J.alpha + off : nullptr;
-    rs.i = ok && doI ? J.img + po + off : nullptr;
-    rs.f = ok && doF ? J.fg_in + po + off : nullptr;
-    rs.b = ok && doF ? J.bg_in + po + off : nullptr;
+    const long long oi = (long long)y * J.ipitch, of = (long long)y * J.fpitch;
+    rs.a = ok && doA ? J.alpha + oi : nullptr;
+    rs.i = ok && doI ? J.img + ch * J.istride + oi : nullptr;
+    rs.f = ok && doF ? J.fg_in + ch * J.fstride + of : nullptr;
+    rs.b = ok && doF ? J.bg_in + ch * J.fstride + of : nullptr;
     rs.s = sbase + 4u * unsigned(G::OFF_A + (r + K) * 32);
     rs.r = r;
     return rs;
@@ -190,6 +189,7 @@ struct StepCtx {
     float* my_stream;  // this band's stream (column 0)
     float* FO;
     float* BO;
+    int opitch;
     float eps, omega;
 };
 
@@ -283,7 +283,7 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
         bool ok = true;
         if (G) ok = xf >= OW - 1 && xf < w && yf >= 0 && yf < h;
         if (ok) {
-            const long long off = (long long)yf * w + (xf - (OW - 1)) + col;
+            const long long off = (long long)yf * x_.opitch + (xf - (OW - 1)) + col;
             const float* o = sm + Gm::OFF_O + jf * OW + col;
             x_.FO[off] = o[0];
             x_.BO[off] = o[32 * OW];
@@ -293,7 +293,7 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
             const int x0 = (w - 1) & ~(OW - 1);
             const int ye = y0 + je - (K - 1);
             if (je >= 0 && je < 32 && ye >= 0 && ye < h && lane < w - x0) {
-                const long long off = (long long)ye * w + x0 + lane;
+                const long long off = (long long)ye * x_.opitch + x0 + lane;
                 const float* o = sm + Gm::OFF_O + je * OW + lane;
                 x_.FO[off] = o[0];
                 x_.BO[off] = o[32 * OW];
@@ -353,8 +353,9 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     cx.has_down = q < J.nb - 1;
     cx.Umax = Umax;
     cx.my_stream = J.stream + size_t(sid) * slen;
-    cx.FO = J.fg_out + (long long)ch * J.pstride;
-    cx.BO = J.bg_out + (long long)ch * J.pstride;
+    cx.FO = J.fg_out + (long long)ch * J.ostride;
+    cx.BO = J.bg_out + (long long)ch * J.ostride;
+    cx.opitch = J.opitch;
     cx.eps = eps;
     cx.omega = omega;
 
@@ -457,9 +458,9 @@ cudaError_t launch_sweep_k(const SweepJob* jobs_dev, const int2* order_dev, int 
     return cudaGetLastError();
 }
 
-__global__ void stream_fill_kernel(const SweepJob* __restrict__ jobs, int K) {
+__global__ void stream_fill_kernel(const SweepJob* __restrict__ jobs, int K, bool full) {
     const SweepJob J = jobs[blockIdx.y];
-    const size_t n = size_t(3) * J.nb * sweep_stream_len(J.w, K) / 4;  // float4 count
+    const size_t n = size_t(J.nb) * (full ? sweep_full_stream_len(J.w, K) : 3 * sweep_stream_len(J.w, K)) / 4;
     float4* p = reinterpret_cast<float4*>(J.stream);
     const float s = __uint_as_float(kStreamSentinel);
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
@@ -468,10 +469,11 @@ __global__ void stream_fill_kernel(const SweepJob* __restrict__ jobs, int K) {
 
 }  // namespace
 
-cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, size_t max_floats, cudaStream_t s) {
+cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, bool full, size_t max_floats,
+                               cudaStream_t s) {
     if (njobs <= 0) return cudaSuccess;
     const int gx = int(std::min<size_t>(std::max<size_t>((max_floats / 4 + 255) / 256, 1), 64));
-    stream_fill_kernel<<<dim3(gx, njobs), 256, 0, s>>>(jobs_dev, K);
+    stream_fill_kernel<<<dim3(gx, njobs), 256, 0, s>>>(jobs_dev, K, full);
     return cudaGetLastError();
 }
 

@@ -273,3 +273,41 @@ def test_batch_equals_single_bitwise(fgm, cuda):
     for im, al, (f, b) in zip(imgs, alps, outs):
         f1, b1 = fgm.ml_foreground_background_cuda(im, al, fgm.BASELINE_PARAMS)
         assert torch.equal(f, f1) and torch.equal(b, b1)
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(iters_high=1), dict(iters_high=3), dict(iters_high=5)])
+def test_sweep_kernels_agree_bitwise(fgm, cuda, oracle_mod, kw):
+    # per-(band, channel) warps vs full-channel warps with passed coefficients:
+    # the same arithmetic, so the same bits
+    from paper_2006_14970_b200 import synth
+
+    p = params_from(fgm, oracle_mod.Params(**kw))
+    imgs, alps = [], []
+    for i, (w, h) in enumerate([(700, 300), (257, 513), (96, 64), (1000, 33)]):
+        im, al = synth.make_composite(w, h, 300 + i, 4, 3.0)
+        imgs.append(im.to(cuda))
+        alps.append(al.to(cuda))
+    try:
+        fgm.set_sweep_mode(1)
+        a = fgm.batch_solve_cuda(imgs, alps, p)
+        fgm.set_sweep_mode(2)
+        b = fgm.batch_solve_cuda(imgs, alps, p)
+    finally:
+        fgm.set_sweep_mode(0)
+    for (fa, ba), (fb, bb) in zip(a, b):
+        assert torch.equal(fa, fb) and torch.equal(ba, bb)
+
+
+def test_full_channel_kernel_vs_oracle(fgm, cuda, orc, oracle_mod):
+    from paper_2006_14970_b200 import synth
+
+    img, a = synth.make_composite(333, 517, 17, 4, 3.0)
+    try:
+        fgm.set_sweep_mode(2)
+        for p in (oracle_mod.Params(), oracle_mod.REFERENCE_DEFAULTS, oracle_mod.Params(iters_high=3)):
+            f, b = gpu_solve(fgm, cuda, img.numpy(), a.numpy(), p)
+            of, ob = orc.ml_solve(img.double().numpy(), a.double().numpy(), p)
+            assert_close("fg", f, of)
+            assert_close("bg", b, ob)
+    finally:
+        fgm.set_sweep_mode(0)
