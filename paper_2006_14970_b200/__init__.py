@@ -83,9 +83,10 @@ def _load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_build.LIB):
-        raise ImportError(f"fgmatte_b200 CUDA library not built: {_build.LIB} (run __graft_entry__.build())")
-    L = C.CDLL(_build.LIB)
+    path = os.environ.get("FGMATTE_B200_LIB", _build.LIB)  # tuning variants (tools/)
+    if not os.path.exists(path):
+        raise ImportError(f"fgmatte_b200 CUDA library not built: {path} (run __graft_entry__.build())")
+    L = C.CDLL(path)
     fp, ip, vp = C.POINTER(C.c_float), C.POINTER(C.c_int), C.c_void_p
     P = C.POINTER(_CParams)
     L.fgm_last_error.restype = C.c_char_p

@@ -123,6 +123,28 @@ __device__ __forceinline__ Coef1 pixel_coef1(float a, float aL, float aR, float 
     return co;
 }
 
+// pixel_coef1 with the left edge weight given (the right edge weight of the
+// left neighbour: |a - aL| is exactly symmetric, so it is the same value).
+__device__ __forceinline__ Coef1 pixel_coef1_dl(float a, float dL, float aR, float aU, float aD, float I, float eps,
+                                                float omega) {
+    Coef1 co;
+    co.dL = dL;
+    co.dR = edge_weight(a, aR, eps, omega);
+    co.dU = edge_weight(a, aU, eps, omega);
+    co.dD = edge_weight(a, aD, eps, omega);
+    const float S = __fadd_rn(__fadd_rn(__fadd_rn(co.dL, co.dR), co.dU), co.dD);
+    const float u0 = a, u1 = __fsub_rn(1.0f, a);
+    const float u00 = __fmul_rn(u0, u0), u11 = __fmul_rn(u1, u1), u01 = __fmul_rn(u0, u1);
+    const float iS = rcp_approx(S);
+    const float iD = rcp_approx(__fadd_rn(__fadd_rn(u00, u11), S));
+    co.A = __fmul_rn(iD, __fmaf_rn(u11, iS, 1.0f));
+    co.A2 = __fmul_rn(iD, __fmaf_rn(u00, iS, 1.0f));
+    co.Bc = -__fmul_rn(iD, __fmul_rn(u01, iS));
+    co.pI = __fmul_rn(__fmul_rn(iD, u0), I);
+    co.qI = __fmul_rn(__fmul_rn(iD, u1), I);
+    return co;
+}
+
 // Alpha-only part shared by the three channels of a pixel: the Coef1 fields
 // without the image term; p = u0/D, q = u1/D multiply I_c per channel.  Bn is
 // -Bc, kept positive (a product, never a sign-flipped NaN: these values travel

@@ -15,6 +15,7 @@ struct ResampleJob {
     long long spstride, dpstride;  // plane strides in floats
     double sx, sy;                 // double(sw)/double(dw), double(sh)/double(dh) (image.cpp:73)
     int tile_base;                 // first tile of this job in the launch's flat tile space
+    int idx32;                     // every src/dst element index fits in int32 (set by the host)
 };
 
 // ---- K4: coarse levels, one CTA per image, shared-memory resident ---------
@@ -82,6 +83,10 @@ inline size_t sweep_stream_floats(int w, int h, int K) {
 // Tiles of 128 x 8 destination pixels; total_tiles = sum over jobs.
 int resample_tiles(int dw, int dh);
 cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s);
+// F/B upsample (sw <= dw, sh <= dh, six planes): shared-memory staged tiles
+int upsample_tiles(int dw, int dh);
+cudaError_t launch_upsample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s);
+bool upsample_ok(int sw, int sh, int dw, int dh);  // scale within the staged window
 cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float omega, cudaStream_t s);
 // order_dev[t] = (job, 3 * band + channel) of ticket t, band-major across jobs.
 cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands, unsigned* ticket,

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "fgm_device.cuh"
 #include "fgm_internal.h"
@@ -25,42 +26,47 @@ namespace fgm {
 constexpr int kResCols = 128;
 constexpr int kResRows = 8;
 
-template <int NP>
+// Index type Ix: int when every element index of the job fits in 32 bits
+// (one IMAD.WIDE per address instead of 64-bit arithmetic), else long long.
+template <int NP, typename Ix>
 __device__ __forceinline__ void resample_tile(const ResampleJob& J, int x, int ybase, const Tap* tys) {
     if (x >= J.dw) return;
     const int yend = min(kResRows, J.dh - ybase);
+    const float* __restrict__ src = J.src;
+    float* __restrict__ dst = J.dst;
+    const Ix sps = Ix(J.spstride), dps = Ix(J.dpstride), sp = Ix(J.spitch), dp = Ix(J.dpitch);
+    Ix o = Ix(ybase) * dp + x;
     if (J.sw == J.dw && J.sh == J.dh) {  // resize to the same size: unclamped copy
-        for (int r = 0; r < yend; ++r) {
-            const long long is = (long long)(ybase + r) * J.spitch + x, id = (long long)(ybase + r) * J.dpitch + x;
+        Ix is = Ix(ybase) * sp + x;
+        for (int r = 0; r < yend; ++r, is += sp, o += dp) {
             float v[NP];
 #pragma unroll
-            for (int p = 0; p < NP; ++p) v[p] = __ldg(J.src + p * J.spstride + is);
+            for (int p = 0; p < NP; ++p) v[p] = __ldg(src + (p * sps + is));
 #pragma unroll
-            for (int p = 0; p < NP; ++p) J.dst[p * J.dpstride + id] = v[p];
+            for (int p = 0; p < NP; ++p) dst[p * dps + o] = v[p];
         }
         return;
     }
     const Tap tx = make_tap_s(x, J.sw, J.sx);
-    for (int r = 0; r < yend; ++r) {
+    const int dx = tx.i1 - tx.i0;
+    for (int r = 0; r < yend; ++r, o += dp) {
         const Tap ty = tys[r];
-        const long long r0 = (long long)ty.i0 * J.spitch, r1 = (long long)ty.i1 * J.spitch;
-        const long long o = (long long)(ybase + r) * J.dpitch + x;
-        float a[NP], b[NP], c[NP], d[NP];
+        const Ix a0 = Ix(ty.i0) * sp + tx.i0, c0 = Ix(ty.i1) * sp + tx.i0;
+        float v[NP][4];
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            const float* s = J.src + p * J.spstride;
-            a[p] = __ldg(s + r0 + tx.i0);
-            b[p] = __ldg(s + r0 + tx.i1);
-            c[p] = __ldg(s + r1 + tx.i0);
-            d[p] = __ldg(s + r1 + tx.i1);
+            const float* s = src + p * sps;
+            v[p][0] = __ldg(s + a0);
+            v[p][1] = __ldg(s + a0 + dx);
+            v[p][2] = __ldg(s + c0);
+            v[p][3] = __ldg(s + c0 + dx);
         }
 #pragma unroll
-        for (int p = 0; p < NP; ++p) J.dst[p * J.dpstride + o] = bilerp(a[p], b[p], c[p], d[p], tx.t, ty.t);
+        for (int p = 0; p < NP; ++p) dst[p * dps + o] = bilerp(v[p][0], v[p][1], v[p][2], v[p][3], tx.t, ty.t);
     }
 }
 
-template <>
-__device__ __forceinline__ void resample_tile<0>(const ResampleJob& J, int x, int ybase, const Tap* tys) {
+__device__ __forceinline__ void resample_tile_generic(const ResampleJob& J, int x, int ybase, const Tap* tys) {
     if (x >= J.dw) return;  // generic plane count (fgm_resize_f32)
     const int yend = min(kResRows, J.dh - ybase);
     const bool ident = J.sw == J.dw && J.sh == J.dh;
@@ -100,13 +106,178 @@ __global__ void __launch_bounds__(kResCols) resample_kernel(const ResampleJob* _
         if (threadIdx.x < kResRows && ybase + threadIdx.x < J.dh)
             tys[threadIdx.x] = make_tap_s(ybase + threadIdx.x, J.sh, J.sy);
         __syncthreads();
-        switch (J.nplanes) {
-            case 1: resample_tile<1>(J, x, ybase, tys); break;
-            case 3: resample_tile<3>(J, x, ybase, tys); break;
-            case 6: resample_tile<6>(J, x, ybase, tys); break;
-            default: resample_tile<0>(J, x, ybase, tys); break;
+        if (J.idx32) {
+            switch (J.nplanes) {
+                case 1: resample_tile<1, int>(J, x, ybase, tys); break;
+                case 3: resample_tile<3, int>(J, x, ybase, tys); break;
+                case 6: resample_tile<6, int>(J, x, ybase, tys); break;
+                default: resample_tile_generic(J, x, ybase, tys); break;
+            }
+        } else {
+            switch (J.nplanes) {
+                case 1: resample_tile<1, long long>(J, x, ybase, tys); break;
+                case 3: resample_tile<3, long long>(J, x, ybase, tys); break;
+                case 6: resample_tile<6, long long>(J, x, ybase, tys); break;
+                default: resample_tile_generic(J, x, ybase, tys); break;
+            }
         }
     }
+}
+
+// ----------------------------------------------------------------------------
+// Upsampling of the six F/B planes from the previous level, for scales
+// sw/dw, sh/dh <= kUpMaxScale (level sizes grow by ~2x; larger scales take the
+// generic resample kernel).  A tile of 8 x 128 outputs reads at most
+// kUpSR x kUpSC source texels per plane.  Each block double-buffers the
+// staged windows of two consecutive tiles in shared memory (cp.async), so the
+// next tile's loads overlap this tile's interpolation; every output takes its
+// four taps from shared memory with compile-time plane offsets.  Same
+// arithmetic as resample_tile (bitwise identical results).
+constexpr int kUpCols = 128, kUpRows = 8, kUpThreads = 128;
+constexpr double kUpMaxScale = 0.625;
+constexpr int kUpSR = 8;   // ceil(7 * 0.625) + 3
+constexpr int kUpSC = 83;  // ceil(127 * 0.625) + 3
+constexpr int kUpPlane = kUpSR * kUpSC;
+constexpr int kUpBuf = 6 * kUpPlane;
+
+__device__ __forceinline__ void cp_async_f32(unsigned sdst, const float* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sdst), "l"(gsrc) : "memory");
+}
+
+struct UpTile {
+    int job, y0, x0, nrows, ncols, r0, c0, nr, nc;  // nr x nc: staged source window
+};
+
+// Tile geometry and source window; `job` advances monotonically per block.
+__device__ __forceinline__ UpTile up_tile(const ResampleJob* __restrict__ jobs, int njobs, int gt, int job) {
+    while (job + 1 < njobs && jobs[job + 1].tile_base <= gt) ++job;
+    const ResampleJob& J = jobs[job];
+    const int tile = gt - J.tile_base;
+    const int tcols = (J.dw + kUpCols - 1) / kUpCols;
+    const int tyi = tile / tcols, txi = tile - tyi * tcols;
+    UpTile t;
+    t.job = job;
+    t.y0 = tyi * kUpRows;
+    t.x0 = txi * kUpCols;
+    t.nrows = min(kUpRows, J.dh - t.y0);
+    t.ncols = min(kUpCols, J.dw - t.x0);
+    t.r0 = make_tap_s(t.y0, J.sh, J.sy).i0;
+    t.c0 = make_tap_s(t.x0, J.sw, J.sx).i0;
+    // exact window: up to the last row's / column's i1
+    t.nr = make_tap_s(t.y0 + t.nrows - 1, J.sh, J.sy).i1 - t.r0 + 1;
+    t.nc = make_tap_s(t.x0 + t.ncols - 1, J.sw, J.sx).i1 - t.c0 + 1;
+    return t;
+}
+
+// Issue the cp.async loads of a tile's window (rows r0.., columns c0..,
+// clamped to the source) and its row taps (threads 0..7) into buffer b.
+__device__ __forceinline__ void up_stage(const ResampleJob& J, const UpTile& t, unsigned sbuf, Tap* tys, int tid) {
+    const int nr = t.nr, nc = t.nc;  // <= kUpSR x kUpSC at scales <= kUpMaxScale
+    const int sp = J.spitch;
+    const long long sps = J.spstride;
+    const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+        const float* sp0 = J.src + p * sps + (long long)t.r0 * sp + t.c0;
+        for (int r = warp; r < nr; r += kUpThreads / 32) {
+            const float* srow = sp0 + (long long)r * sp;
+            const unsigned drow = sbuf + 4u * unsigned(p * kUpPlane + r * kUpSC);
+            for (int c = lane; c < nc; c += 32) cp_async_f32(drow + 4u * c, srow + c);
+        }
+    }
+    if (tid < t.nrows) tys[tid] = make_tap_s(t.y0 + tid, J.sh, J.sy);
+}
+
+__global__ void __launch_bounds__(kUpThreads) upsample_kernel(const ResampleJob* __restrict__ jobs, int njobs,
+                                                              int total_tiles) {
+    extern __shared__ float4 up_sm4[];
+    float* sm = reinterpret_cast<float*>(up_sm4);
+    const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sm));
+    __shared__ Tap tys[2][kUpRows];
+    const int tid = threadIdx.x;
+    int gt = blockIdx.x;
+    if (gt >= total_tiles) return;
+    UpTile cur = up_tile(jobs, njobs, gt, 0);
+    up_stage(jobs[cur.job], cur, sbase, tys[0], tid);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int it = 0;; ++it) {
+        const int b = it & 1;
+        const int gn = gt + gridDim.x;
+        UpTile nxt = cur;
+        if (gn < total_tiles) {  // stage the next tile into the other buffer
+            nxt = up_tile(jobs, njobs, gn, cur.job);
+            up_stage(jobs[nxt.job], nxt, sbase + 4u * unsigned((b ^ 1) * kUpBuf), tys[b ^ 1], tid);
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;" ::: "memory");
+        __syncthreads();  // this tile's window and taps are visible
+        {
+            // thread = (lane l, row pair rp): columns x0 + l + 32i (i < 4), rows
+            // 2rp, 2rp+1.  Lanes read neighbouring (or equal) staged words:
+            // no bank conflicts; stores are 128-byte warp rows.
+            const ResampleJob& J = jobs[cur.job];
+            const int l = tid & 31, rp = tid >> 5;
+            int sa[4], dx[4];
+            float tx[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const Tap t = make_tap_s(min(cur.x0 + l + 32 * i, J.dw - 1), J.sw, J.sx);
+                sa[i] = t.i0 - cur.c0;
+                dx[i] = t.i1 - t.i0;
+                tx[i] = t.t;
+            }
+            const float* buf = sm + b * kUpBuf;
+            const long long dps = J.dpstride;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int rr = 2 * rp + h;
+                if (rr >= cur.nrows) break;
+                const Tap ty = tys[b][rr];
+                const float* ra = buf + (ty.i0 - cur.r0) * kUpSC;
+                const float* rc = buf + (ty.i1 - cur.r0) * kUpSC;
+                float* d = J.dst + (long long)(cur.y0 + rr) * J.dpitch + cur.x0 + l;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (l + 32 * i >= cur.ncols) break;
+#pragma unroll
+                    for (int p = 0; p < 6; ++p) {
+                        const float* a = ra + p * kUpPlane + sa[i];
+                        const float* c = rc + p * kUpPlane + sa[i];
+                        d[p * dps + 32 * i] = bilerp(a[0], a[dx[i]], c[0], c[dx[i]], tx[i], ty.t);
+                    }
+                }
+            }
+        }
+        __syncthreads();  // buffer b is free for the tile after next
+        if (gn >= total_tiles) break;
+        gt = gn;
+        cur = nxt;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+int upsample_tiles(int dw, int dh) { return ((dw + kUpCols - 1) / kUpCols) * ((dh + kUpRows - 1) / kUpRows); }
+
+cudaError_t launch_upsample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s) {
+    if (njobs <= 0 || total_tiles <= 0) return cudaSuccess;
+    constexpr size_t smem = size_t(2) * kUpBuf * sizeof(float);
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        cudaError_t e = cudaFuncSetAttribute(upsample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upsample_kernel, kUpThreads, smem);
+        per_sm = std::max(per_sm, 1);
+    }
+    const int gx = int(std::min<long long>(total_tiles, (long long)sms * per_sm));
+    upsample_kernel<<<gx, kUpThreads, smem, s>>>(jobs_dev, njobs, int(total_tiles));
+    return cudaGetLastError();
+}
+
+bool upsample_ok(int sw, int sh, int dw, int dh) {
+    return !(sw == dw && sh == dh) && double(sw) / double(dw) <= kUpMaxScale &&
+           double(sh) / double(dh) <= kUpMaxScale;
 }
 
 int resample_tiles(int dw, int dh) { return ((dw + kResCols - 1) / kResCols) * ((dh + kResRows - 1) / kResRows); }

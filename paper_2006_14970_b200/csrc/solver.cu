@@ -181,6 +181,7 @@ ResampleJob rjob(const float* src, float* dst, int sw, int sh, int dw, int dh, i
     r.dpstride = (long long)dpitch * dh;
     r.sx = double(sw) / double(dw);  // make_taps' scale, image.cpp:73
     r.sy = double(sh) / double(dh);
+    r.idx32 = (long long)np * std::max(r.spstride, r.dpstride) < (1ll << 31) ? 1 : 0;
     return r;
 }
 
@@ -365,7 +366,7 @@ bool use_full_kernel(int total_bands, int K) {
     return g_sweep_mode == 2;
 }
 
-enum LaunchKind { kCoarse, kResample, kSweep, kCopy };
+enum LaunchKind { kCoarse, kResample, kUpsample, kSweep, kCopy };
 struct LaunchRec {
     LaunchKind kind;
     int K, njobs, total_bands;
@@ -441,9 +442,9 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
 
     // ---- big levels, aligned so that every image's top level is step J-1 --
     for (int j = 0; j < J; ++j) {
-        std::vector<ResampleJob> rj;
+        std::vector<ResampleJob> rj, uj;  // resample (I/alpha) and upsample (F/B) jobs
         long long max_rows = 0;
-        double rbytes = 0;
+        double rbytes = 0, ubytes = 0;
         struct Active {
             Plan* P;
             int l;
@@ -464,9 +465,16 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 rj.push_back(rjob(P.io.alpha, P.lvlIA + 3 * pps, P.io.W, P.io.H, L.w, L.h, 1, P.io.W, pp));
                 rbytes += 4.0 * 4 * (double(px) + std::min<double>(double(fpx), 4.0 * px));
             }
-            // the previous level's output: the coarse kernel's or a sweep's (both pitched)
-            rj.push_back(rjob(P.fbOut, P.fbInit, Lp.w, Lp.h, L.w, L.h, 6, level_pitch(Lp.w), pp));
-            rbytes += 4.0 * 6 * (double(px) + double(ppx));
+            // the previous level's output: the coarse kernel's or a sweep's (both
+            // pitched); levels grow, so this is an upsample (staged kernel)
+            const ResampleJob fj = rjob(P.fbOut, P.fbInit, Lp.w, Lp.h, L.w, L.h, 6, level_pitch(Lp.w), pp);
+            if (upsample_ok(Lp.w, Lp.h, L.w, L.h)) {
+                uj.push_back(fj);
+                ubytes += 4.0 * 6 * (double(px) + double(ppx));
+            } else {
+                rj.push_back(fj);
+                rbytes += 4.0 * 6 * (double(px) + double(ppx));
+            }
 
         }
         if (act.empty()) continue;
@@ -474,7 +482,13 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             r.tile_base = int(max_rows);
             max_rows += resample_tiles(r.dw, r.dh);
         }
-        launches.push_back({kResample, 0, int(rj.size()), 0, false, st.push(rj), 0, 0, max_rows, rbytes});
+        if (!rj.empty()) launches.push_back({kResample, 0, int(rj.size()), 0, false, st.push(rj), 0, 0, max_rows, rbytes});
+        long long up_tiles = 0;
+        for (auto& r : uj) {
+            r.tile_base = int(up_tiles);
+            up_tiles += upsample_tiles(r.dw, r.dh);
+        }
+        if (!uj.empty()) launches.push_back({kUpsample, 0, int(uj.size()), 0, false, st.push(uj), 0, 0, up_tiles, ubytes});
         size_t max_passes = 0;
         for (auto& a : act) max_passes = std::max(max_passes, passes_for(a.P->lv[size_t(a.l)].iters).size());
         for (size_t pi = 0; pi < max_passes; ++pi) {
@@ -576,6 +590,12 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 ProfScope ps(s, 1, r.bytes);
                 ck(launch_resample(reinterpret_cast<const ResampleJob*>(djobs + r.job_off), r.njobs, r.max_rows, s),
                    "resample_kernel");
+                break;
+            }
+            case kUpsample: {
+                ProfScope ps(s, 1, r.bytes);
+                ck(launch_upsample(reinterpret_cast<const ResampleJob*>(djobs + r.job_off), r.njobs, r.max_rows, s),
+                   "upsample_kernel");
                 break;
             }
             case kSweep: {

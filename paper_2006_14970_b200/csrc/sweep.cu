@@ -21,21 +21,26 @@
 // column, and band q+1 polls each 16-column chunk until no word is the
 // sentinel (outputs are clamped to [0, 1], never NaN).  Each word validates
 // itself, so no fences are needed on either side; the next chunk is fetched
-// one chunk ahead and only re-polled if it was not complete yet.
+// one chunk ahead and re-polled once per group while incomplete.
 //
 // The three colour channels share only alpha (the 2x2 matrix is common to all
 // channels, multilevel.hpp:37-43), so each (band, channel) is an independent
-// warp: it recomputes the alpha-only coefficients (pixel_coef1) and runs the
-// F_c / B_c recurrence (pixel_apply1) of its channel.
+// warp: it computes the alpha-only coefficients of its pixels and runs the
+// F_c / B_c recurrence (pixel_apply1) of its channel.  The left edge weight
+// of a pixel is the right edge weight of the pixel the same slot updated one
+// step earlier (|a - b| is exactly symmetric), so only three are computed.
 //
 // Memory: each warp streams its band's rows of alpha, I_c and the initial F_c,
 // B_c through per-row shared-memory rings of 32 columns, filled by cp.async
-// kLead columns ahead of use; element (row r, column x) sits at ring column
-// x mod 32, so the diagonal reads of a step hit 32 distinct banks and every
-// ring row of a lane is a compile-time offset from its alpha row.  Outputs go
-// through a 16-column ring per row and leave as coalesced 64-byte row segments
-// (two rows per step) once complete.  Steps run in groups of four: loads,
-// stream chunks and the border/fast decision are handled once per group.
+// 16-byte blocks M groups ahead of use.  Element (row r, column x) sits at
+// ring column x mod 32; the first MIR columns are mirrored after column 31, so
+// every read of a step is  lane_base + 4*c + (compile-time offset)  with one
+// c = (t - lane - SH) mod 32 per step -- no per-access index arithmetic.  Rows
+// are RS = 32 + MIR floats apart: the diagonal reads of a step hit banks
+// (RS - 1) * lane + const, all distinct since RS - 1 is odd.  Outputs go
+// through a 16-column ring per row and leave as 64-byte row segments (two
+// rows per step) once complete.  Steps run in groups of four: loads, stream
+// chunks and the border/fast decision are handled once per group.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -48,6 +53,13 @@ namespace {
 
 __device__ __forceinline__ void cp_async16(unsigned sdst, const float* gsrc, int src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sdst), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+// Predicated 16-byte copy without zero-fill (a predicate, not a branch).
+__device__ __forceinline__ void cp_async16_if(unsigned sdst, const float* gsrc, unsigned pred) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p cp.async.cg.shared.global [%0], [%1], 16;\n}" ::"r"(sdst),
+        "l"(gsrc), "r"(pred)
+        : "memory");
 }
 __device__ __forceinline__ void cp_async4(unsigned sdst, const float* gsrc, int src_bytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sdst), "l"(gsrc), "r"(src_bytes) : "memory");
@@ -65,53 +77,79 @@ __device__ __forceinline__ float4 ld_relaxed_v4(const float* p) {
                  : "memory");
     return v;
 }
+// Boundary-stream stores need no ordering against this warp's other memory
+// operations (every word validates itself), hence no "memory" clobber: the
+// compiler may keep scheduling shared-memory loads across them.
 __device__ __forceinline__ void st_relaxed_v4(float* p, float4 v) {
     asm volatile("st.relaxed.gpu.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-                 "f"(v.w)
-                 : "memory");
+                 "f"(v.w));
 }
 __device__ __forceinline__ void st_relaxed_v2(float* p, float2 v) {
-    asm volatile("st.relaxed.gpu.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+    asm volatile("st.relaxed.gpu.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y));
 }
+// The dynamic shared memory of the sweep kernel, addressed by float index:
+// the compiler sees shared-space accesses (LDS/STS with the compile-time part
+// of an index folded into the instruction) and orders them against
+// __syncwarp and the cp.async waits.
+extern __shared__ float4 sweep_sm4[];
+__device__ __forceinline__ float* smf() { return reinterpret_cast<float*>(sweep_sm4); }
+__device__ __forceinline__ float lds(int i) { return smf()[i]; }
+__device__ __forceinline__ void sts(int i, float v) { smf()[i] = v; }
+__device__ __forceinline__ void sts4(int i, float4 v) { reinterpret_cast<float4*>(smf() + i)[0] = v; }
+__device__ __forceinline__ void stg(float* p, float v) { __stcg(p, v); }
 __device__ __forceinline__ bool is_sentinel(float v) { return __float_as_uint(v) == kStreamSentinel; }
 
-// Shared-memory geometry of one (band, channel) warp, in floats.  Alpha row r
-// (relative to the band) sits at OFF_A + (r + K) * 32; image row r at
-// OFF_I + (r + K - 1) * 32; initial F_c / B_c row r at OFF_F / OFF_B + r * 32.
+// Shared-memory geometry of one (band, channel) warp, in floats.
+//
+// Ring window.  In row-time tau = x + r (band row r, column x) the reads of
+// step t cover alpha tau in [t-2K+2, t+2] (the next step's pixels and their
+// four neighbours), image [t-2K+3, t+1] and the initial F/B [t, t+1].  Loads
+// of 4-column blocks are issued at the end of each 4-step group with a lead
+// L = 4M - 1 + W1 (W1 = the window's reach past the group), so a group waits
+// only for loads issued M groups earlier; the live span 4M + 3 + W0 + W1 must
+// fit in the 32 ring columns (static_asserts below).
 template <int K>
 struct Geom {
-    static constexpr int kLead = K <= 2 ? 20 : 16;  // prefetch lead in columns
-    static constexpr int NA = 33 + K;               // alpha rows -K .. 32
-    static constexpr int NI = 31 + K;               // image rows -(K-1) .. 31
-    static constexpr int NF = 33;                   // initial F/B rows 0 .. 32
-    static constexpr int OW = 16;                   // output ring columns
+    static constexpr int RW = 32;               // ring columns
+    static constexpr int SH = K - 1;            // read column shift: offsets d + SH >= 0
+    static constexpr int MIR = K <= 2 ? 4 : 8;  // mirrored columns (> largest shifted offset)
+    static constexpr int RS = RW + MIR;         // row stride (floats), 16-byte multiple, RS - 1 odd
+    static constexpr int M = 4;                 // load groups in flight
+    static constexpr int L = 4 * M + 1;         // load lead: 4M - 1 + W1, W1 = 2 (alpha; 1 for the others)
+    static constexpr int NA = 33 + K;           // alpha ring rows: band rows -K .. 32
+    static constexpr int NI = 31 + K;           // image ring rows: band rows -(K-1) .. 31
+    static constexpr int NF = 33;               // F/B ring rows: band rows 0 .. 32
+    static constexpr int OW = 16;               // output ring columns
     static constexpr int OFF_A = 0;
-    static constexpr int OFF_I = OFF_A + NA * 32;
-    static constexpr int OFF_F = OFF_I + NI * 32;
-    static constexpr int OFF_B = OFF_F + NF * 32;
-    static constexpr int OFF_O = OFF_B + NF * 32;  // [plane F/B][lane][OW]
-    static constexpr int OFF_C = OFF_O + 2 * 32 * OW;
+    static constexpr int OFF_I = OFF_A + NA * RS;
+    static constexpr int OFF_F = OFF_I + NI * RS;
+    static constexpr int OFF_B = OFF_F + NF * RS;
+    static constexpr int OFF_O = OFF_B + NF * RS;  // [plane F/B][orow(j)][OW]
+    static constexpr int OPL = 33 * OW;
+    static constexpr int OFF_C = OFF_O + 2 * OPL;
     static constexpr int CH = kChunk * K * 2;  // one boundary-stream chunk: [u][k][F,B]
     static constexpr int CH4 = CH / 4;         // float4 per chunk (<= 32: one per lane)
     static constexpr int TOTAL = OFF_C + CH;
-    static constexpr int dI = OFF_I - OFF_A - 32;      // image row r - alpha row r
-    static constexpr int dF = OFF_F - OFF_A - 32 * K;  // F row r - alpha row r
-    static constexpr int dB = OFF_B - OFF_A - 32 * K;  // B row r - alpha row r
-    // live alpha/image window is [t-2K+2, t+2] in row-time, plus the lead
-    static_assert(kLead + 2 * K + 6 <= 32, "ring too small for the prefetch lead");
-    static_assert(kLead % 4 == 0, "lead must be whole 16-byte blocks");
+    static_assert(L + (2 * K - 2) + 4 <= RW, "alpha ring too small for its lead");
+    static_assert(2 + SH <= MIR && MIR % 4 == 0 && RS % 4 == 0, "mirror too narrow");
     static_assert(CH % 4 == 0 && CH4 <= 32, "a chunk is at most one float4 per lane");
 };
 
+// output ring row of band row j (a padding row after row 15: the diagonal
+// writes and the two-row flush reads hit distinct banks)
+__device__ __forceinline__ constexpr int orow(int j) { return j + (j >> 4); }
+
 // The global rows a lane streams into its rings (its own row and, for some
-// lanes, one extra row: alpha -K..-1, image -(K-1)..-1, F/B 32).
+// lanes, one extra row: alpha -K..-1 and 32, image -(K-1)..-1, F/B 32).
+// Ring rows of one band row sit at compile-time offsets from `s` (alpha row
+// r + K, image row r + K - 1, F/B row r); planes the lane does not stream, or
+// rows outside the image, are masked off in `vm` (their ring slots are never
+// read unclamped).
 struct RowSrc {
-    const float* a;  // alpha row (or null)
-    const float* i;  // image row of channel c (or null)
-    const float* f;  // initial F_c row (or null)
-    const float* b;  // initial B_c row (or null)
-    unsigned s;      // shared address of this row's alpha ring
-    int r;           // row relative to the band
+    const float* g[4];  // alpha, image c, F_c, B_c rows (column 0)
+    unsigned s;         // shared address of ring offset 0, ring row r, column 0
+    unsigned vm;        // bit p: plane p is streamed
+    int r;              // row relative to the band
 };
 
 template <int K>
@@ -121,56 +159,130 @@ __device__ __forceinline__ RowSrc make_rowsrc(const SweepJob& J, int ch, int y0,
     RowSrc rs;
     const int y = y0 + r;
     const bool ok = y >= 0 && y < J.h;
-    const long long oi = (long long)y * J.ipitch, of = (long long)y * J.fpitch;
-    rs.a = ok && doA ? J.alpha + oi : nullptr;
-    rs.i = ok && doI ? J.img + ch * J.istride + oi : nullptr;
-    rs.f = ok && doF ? J.fg_in + ch * J.fstride + of : nullptr;
-    rs.b = ok && doF ? J.bg_in + ch * J.fstride + of : nullptr;
-    rs.s = sbase + 4u * unsigned(G::OFF_A + (r + K) * 32);
+    const long long oi = (long long)(ok ? y : 0) * J.ipitch, of = (long long)(ok ? y : 0) * J.fpitch;
+    rs.g[0] = J.alpha + oi;
+    rs.g[1] = J.img + ch * J.istride + oi;
+    rs.g[2] = J.fg_in + ch * J.fstride + of;
+    rs.g[3] = J.bg_in + ch * J.fstride + of;
+    rs.s = sbase + 4u * unsigned(r * G::RS);  // may wrap below sbase: only ever offset back into range
+    rs.vm = ok ? (doA ? 1u : 0u) | (doI ? 2u : 0u) | (doF ? 12u : 0u) : 0u;
     rs.r = r;
     return rs;
 }
 
-// cp.async of block b (columns 4b..4b+3) of one row into its rings.
-template <int K, bool V4>
-__device__ __forceinline__ void row_block(const RowSrc& rs, int b, int w) {
+// Ring offset (floats) of plane p's row r relative to ring row r of offset 0.
+template <int K>
+__device__ __forceinline__ constexpr int plane_off(int p) {
     using G = Geom<K>;
-    const int x0 = 4 * b;
-    if (x0 < 0 || x0 >= w) return;
-    const int nb = min(4, w - x0) * 4;
-    const unsigned sa = rs.s + 4u * unsigned(x0 & 31);
-    auto put = [&](unsigned s, const float* row) {
-        if (!row) return;
-        const float* g = row + x0;
-        if (V4) {
-            cp_async16(s, g, nb);
-        } else {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) cp_async4(s + 4 * i, 4 * i < nb ? g + i : g, 4 * i < nb ? 4 : 0);
-        }
-    };
-    put(sa, rs.a);
-    put(sa + 4u * G::dI, rs.i);
-    put(sa + 4u * G::dF, rs.f);
-    put(sa + 4u * G::dB, rs.b);
+    return p == 0 ? G::OFF_A + K * G::RS : p == 1 ? G::OFF_I + (K - 1) * G::RS : p == 2 ? G::OFF_F : G::OFF_B;
 }
 
-// Coefficients of slot k's pixel at ring column cn (row lane-k).  G: clamp
-// neighbours at the image border.
+// cp.async of the 4-column block at column x0 of every streamed plane of one
+// row into the rings (and into the mirror columns when it lands in the first
+// MIR columns).  Columns past the row end are zero-filled (src-size); blocks
+// outside [0, w) are skipped.
+template <int K, bool V4>
+__device__ __forceinline__ void put_blocks(const RowSrc& rs, int x0, int w) {
+    using G = Geom<K>;
+    if (x0 < 0 || x0 >= w) return;
+    const int nb = min(w - x0, 4) * 4;
+    const int c = x0 & (G::RW - 1);
+    const unsigned sc = rs.s + 4u * c;
+    const bool mir = c < G::MIR;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        if (!(rs.vm & (1u << p))) continue;
+        const float* g = rs.g[p] + x0;
+        const unsigned d = sc + 4u * plane_off<K>(p);
+        if (V4) {
+            cp_async16(d, g, nb);
+            if (mir) cp_async16(d + 4u * G::RW, g, nb);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int ok = 4 * i < nb;
+                cp_async4(d + 4 * i, ok ? g + i : g, ok ? 4 : 0);
+                if (mir) cp_async4(d + 4u * G::RW + 4 * i, ok ? g + i : g, ok ? 4 : 0);
+            }
+        }
+    }
+}
+
+// The blocks of one row issued at the end of group t4 (lead L).
+template <int K, bool V4>
+__device__ __forceinline__ void issue_row(const RowSrc& rs, int t4, int w) {
+    put_blocks<K, V4>(rs, (t4 + 4 + Geom<K>::L - rs.r) & ~3, w);
+}
+
+// Interior groups of 16-byte-aligned jobs: every lane's block is inside
+// [0, w), so no range checks and no zero-fill; the per-lane plane mask and
+// the mirror copy become instruction predicates.  MASK: compile-time plane
+// mask (15 for a lane's own row of an interior band), else rs.vm.
+template <int K, unsigned MASK>
+__device__ __forceinline__ void issue_row_fast(const RowSrc& rs, int t4) {
+    using G = Geom<K>;
+    const unsigned x0 = unsigned(t4 + 4 + G::L - rs.r) & ~3u;  // >= 0 in interior groups
+    const unsigned c = x0 & (G::RW - 1);
+    const unsigned sc = rs.s + 4u * c;
+    const unsigned mir = c < unsigned(G::MIR) ? 1u : 0u;
+    const unsigned vm = MASK ? MASK : rs.vm;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const float* g = rs.g[p] + x0;
+        const unsigned d = sc + 4u * plane_off<K>(p);
+        const unsigned on = (vm >> p) & 1u;
+        cp_async16_if(d, g, on);
+        cp_async16_if(d + 4u * G::RW, g, on & mir);
+    }
+}
+
+// Everything issued "before group t0".
+template <int K, bool V4>
+__device__ __forceinline__ void prologue_row(const RowSrc& rs, int t0, int w) {
+    const int last = (t0 + Geom<K>::L - rs.r) & ~3;  // the block issued at the end of group t0 - 4
+    for (int x0 = 0; x0 <= last; x0 += 4) put_blocks<K, V4>(rs, x0, w);
+}
+
+// Float offset, from rc = lane_base + c, of ring `off`, ring row lane + row,
+// shifted column offset dp.
+template <int K>
+__device__ __forceinline__ constexpr int ring(int off, int row, int dp) {
+    return off + row * Geom<K>::RS + dp;
+}
+
+// Coefficients of slot k's pixel of the next step (column offset 1 - k from
+// t - lane), its left edge weight `dL` given.  G: clamp neighbours at the
+// image border.
 template <int K, bool G>
-__device__ __forceinline__ Coef1 slot_coef(const float* sm, int aRow, int cn, int k, int x, int y, int w, int h,
-                                           float eps, float omega) {
+__device__ __forceinline__ Coef1 next_coef(int rc, int k, float dL, int x, int y, int w, int h, float eps,
+                                           float omega) {
     using Gm = Geom<K>;
-    const float* ra = sm + aRow - 32 * k;
-    const float a = ra[cn];
-    float aL = ra[(cn - 1) & 31], aR = ra[(cn + 1) & 31], aU = ra[cn - 32], aD = ra[cn + 32];
+    const int dp = 1 - k + Gm::SH;  // shifted column of the pixel
+    const int ar = K - k;           // alpha ring row (relative to lane) of the pixel
+    const float a = lds(rc + ring<K>(Gm::OFF_A, ar, dp));
+    float aR = lds(rc + ring<K>(Gm::OFF_A, ar, dp + 1));
+    float aU = lds(rc + ring<K>(Gm::OFF_A, ar - 1, dp));
+    float aD = lds(rc + ring<K>(Gm::OFF_A, ar + 1, dp));
+    const float I = lds(rc + ring<K>(Gm::OFF_I, K - 1 - k, dp));
     if (G) {
-        if (x <= 0) aL = a;
+        if (x <= 0) dL = eps;  // edge_weight(a, a)
         if (x >= w - 1) aR = a;
         if (y <= 0) aU = a;
         if (y >= h - 1) aD = a;
     }
-    return pixel_coef1(a, aL, aR, aU, aD, ra[Gm::dI + cn], eps, omega);
+    return pixel_coef1_dl(a, dL, aR, aU, aD, I, eps, omega);
+}
+
+// Coefficients from scratch (the first step of a band: no left pixel yet).
+template <int K>
+__device__ __forceinline__ Coef1 first_coef(int rc, int k, int x, int y, int w, int h, float eps, float omega) {
+    using Gm = Geom<K>;
+    const int dp = 1 - k + Gm::SH;
+    const int ar = K - k;
+    const float a = lds(rc + ring<K>(Gm::OFF_A, ar, dp));
+    const float aL = lds(rc + ring<K>(Gm::OFF_A, ar, dp - 1));
+    const float dL = edge_weight(a, x <= 0 ? a : aL, eps, omega);
+    return next_coef<K, true>(rc, k, dL, x, y, w, h, eps, omega);
 }
 
 template <int K>
@@ -180,14 +292,15 @@ struct LaneState {
     Coef1 co[K];      // coefficients of this step's pixels (computed one step ahead)
 };
 
+template <int K>
 struct StepCtx {
-    const float* sm;
-    float* smw;
+    int lb;  // float index of ring offset 0, row "lane", column 0
+    int ob;  // output ring row orow(lane), column 0
     int lane, y0, w, h;
     bool has_up, has_down;
     int Umax;
     float* my_stream;  // this band's stream (column 0)
-    float* FO;
+    float* FO;  // output planes at band row 0 (image row y0 - (K-1))
     float* BO;
     int opitch;
     float eps, omega;
@@ -196,13 +309,12 @@ struct StepCtx {
 // One wavefront step.  G: a pixel of this step or the next may be on the
 // image border (clamped neighbours) or an output row segment may be partial.
 template <int K, bool G>
-__device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, int tr) {
+__device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_, int tr) {
     using Gm = Geom<K>;
     constexpr int OW = Gm::OW;
     const int lane = x_.lane, y0 = x_.y0, w = x_.w, h = x_.h;
-    const float* sm = x_.sm;
-    const int aRow = Gm::OFF_A + (lane + K) * 32;
-    const int c0 = (tr - lane) & 31;
+    const int c = (tr - lane - Gm::SH) & (Gm::RW - 1);
+    const int rc = x_.lb + c;
 
     float2 recv[K];
 #pragma unroll
@@ -211,9 +323,9 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
         recv[k].y = __shfl_up_sync(kFull, st.outp[k].y, 1);
     }
     if (lane == 0 && x_.has_up && (!G || (tr >= 0 && tr < x_.Umax))) {
-        const float* cn = sm + Gm::OFF_C + (tr % kChunk) * K * 2;
+        const int cn = Gm::OFF_C + (tr % kChunk) * K * 2;
 #pragma unroll
-        for (int k = 0; k < K; ++k) recv[k] = *reinterpret_cast<const float2*>(cn + 2 * k);
+        for (int k = 0; k < K; ++k) recv[k] = make_float2(lds(cn + 2 * k), lds(cn + 2 * k + 1));
     }
 
     float2 nv[K];
@@ -222,17 +334,17 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
     for (int k = 0; k < K; ++k) {
         float2 L = st.outp[k], U = recv[k], R, D;
         if (k == 0) {
-            const float* rf = sm + aRow;
-            R = make_float2(rf[Gm::dF + ((c0 + 1) & 31)], rf[Gm::dB + ((c0 + 1) & 31)]);
-            D = make_float2(rf[Gm::dF + 32 + c0], rf[Gm::dB + 32 + c0]);
+            R = make_float2(lds(rc + ring<K>(Gm::OFF_F, 0, 1 + Gm::SH)), lds(rc + ring<K>(Gm::OFF_B, 0, 1 + Gm::SH)));
+            D = make_float2(lds(rc + ring<K>(Gm::OFF_F, 1, Gm::SH)), lds(rc + ring<K>(Gm::OFF_B, 1, Gm::SH)));
         } else {
             R = recv[k - 1];
             D = st.outp[k - 1];
         }
         if (G) {
             const int x = xs0 - k, y = y0 + lane - k;
-            const float2 self =
-                k == 0 ? make_float2(sm[aRow + Gm::dF + c0], sm[aRow + Gm::dB + c0]) : st.rprev[k > 0 ? k - 1 : 0];
+            const float2 self = k == 0 ? make_float2(lds(rc + ring<K>(Gm::OFF_F, 0, Gm::SH)),
+                                                     lds(rc + ring<K>(Gm::OFF_B, 0, Gm::SH)))
+                                       : st.rprev[k > 0 ? k - 1 : 0];
             if (!(x > 0)) L = self;
             if (!(x < w - 1)) R = self;
             if (!(y > 0)) U = self;
@@ -241,21 +353,22 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
         nv[k] = pixel_apply1(st.co[k], L, R, U, D);
     }
 
-    // coefficients of the next step's pixels (alpha/image rings only)
+    // coefficients of the next step's pixels; dL = this step's dR of the slot
 #pragma unroll
     for (int k = 0; k < K; ++k)
-        st.co[k] = slot_coef<K, G>(sm, aRow, (c0 + 1 - k) & 31, k, xs0 + 1 - k, y0 + lane - k, w, h, x_.eps,
-                                   x_.omega);
+        st.co[k] = next_coef<K, G>(rc, k, st.co[k].dR, xs0 + 1 - k, y0 + lane - k, w, h, x_.eps, x_.omega);
 
-    // output ring (last sweep only)
+    // output ring (last sweep only): column x & 15 == c & 15
     {
-        const int x = xs0 - (K - 1);
         bool ok = true;
-        if (G) ok = x >= 0 && x < w && y0 + lane - (K - 1) >= 0 && y0 + lane - (K - 1) < h;
+        if (G) {
+            const int x = xs0 - (K - 1);
+            ok = x >= 0 && x < w && y0 + lane - (K - 1) >= 0 && y0 + lane - (K - 1) < h;
+        }
         if (ok) {
-            float* o = x_.smw + Gm::OFF_O + lane * OW + (x & (OW - 1));
-            o[0] = nv[K - 1].x;
-            o[32 * OW] = nv[K - 1].y;
+            const int o = x_.ob + (c & (OW - 1));
+            sts(o, nv[K - 1].x);
+            sts(o + Gm::OPL, nv[K - 1].y);
         }
     }
 
@@ -274,29 +387,33 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
 
     __syncwarp();
     // flush completed 16-column output row segments: rows jf (lanes 0-15) and
-    // jf+16 (lanes 16-31), one coalesced 64-byte store per plane each
+    // jf+16 (lanes 16-31), one coalesced 64-byte store per plane each.
+    // Offsets are 32-bit, relative to the band's first output row.
     {
-        const int col = lane & 15;
-        const int jf = ((tr - (K - 1) - (OW - 1)) & (OW - 1)) + (lane & 16);
-        const int xf = tr - jf - (K - 1);  // == 15 mod 16
-        const int yf = y0 + jf - (K - 1);
+        const int col = lane & (OW - 1);
+        const int u = tr - (K - 1) - (OW - 1);
+        const int jf = (u & (OW - 1)) + (lane & 16);
+        const int xs = (u & ~(OW - 1)) - (lane & 16);  // segment start column (xf - 15)
         bool ok = true;
-        if (G) ok = xf >= OW - 1 && xf < w && yf >= 0 && yf < h;
+        if (G) {
+            const int yf = y0 + jf - (K - 1);
+            ok = xs >= 0 && xs + OW - 1 < w && yf >= 0 && yf < h;
+        }
         if (ok) {
-            const long long off = (long long)yf * x_.opitch + (xf - (OW - 1)) + col;
-            const float* o = sm + Gm::OFF_O + jf * OW + col;
-            x_.FO[off] = o[0];
-            x_.BO[off] = o[32 * OW];
+            const int off = jf * x_.opitch + xs + col;
+            const int o = Gm::OFF_O + orow(jf) * OW + col;
+            stg(x_.FO + off, lds(o));
+            stg(x_.BO + off, lds(o + Gm::OPL));
         }
         if (G && ((w - 1) & (OW - 1)) != OW - 1) {  // partial last segment of a row
             const int je = tr - (K - 1) - (w - 1);
             const int x0 = (w - 1) & ~(OW - 1);
             const int ye = y0 + je - (K - 1);
             if (je >= 0 && je < 32 && ye >= 0 && ye < h && lane < w - x0) {
-                const long long off = (long long)ye * x_.opitch + x0 + lane;
-                const float* o = sm + Gm::OFF_O + je * OW + lane;
-                x_.FO[off] = o[0];
-                x_.BO[off] = o[32 * OW];
+                const int off = je * x_.opitch + x0 + lane;
+                const int o = Gm::OFF_O + orow(je) * OW + lane;
+                stg(x_.FO + off, lds(o));
+                stg(x_.BO + off, lds(o + Gm::OPL));
             }
         }
     }
@@ -308,43 +425,47 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
     }
 }
 
-// Poll chunk `u0 / kChunk` of the band above until every word of it is
-// written; leaves it in the chunk buffer.  `v` holds a load issued earlier
-// (one chunk ahead) and is re-polled only while incomplete.
 template <int K>
-__device__ __forceinline__ void acquire_chunk(float4 v, const float* up_stream, int u0, int Umax, int lane,
-                                              float* chunk) {
+__device__ __forceinline__ bool chunk_complete(float4 q, int u0, int Umax, int lane) {
     using G = Geom<K>;
     const int nvalid = min(kChunk, Umax - u0) * K * 2;  // floats
     const bool mine = lane < G::CH4 && 4 * lane < nvalid;
-    auto complete = [&](float4 q) {
-        if (!mine) return true;
-        const int b = 4 * lane;
-        return !(is_sentinel(q.x) || (b + 1 < nvalid && is_sentinel(q.y)) || (b + 2 < nvalid && is_sentinel(q.z)) ||
-                 (b + 3 < nvalid && is_sentinel(q.w)));
-    };
-    while (!__all_sync(kFull, complete(v))) {
+    if (!mine) return true;
+    const int b = 4 * lane;
+    return !(is_sentinel(q.x) || (b + 1 < nvalid && is_sentinel(q.y)) || (b + 2 < nvalid && is_sentinel(q.z)) ||
+             (b + 3 < nvalid && is_sentinel(q.w)));
+}
+
+// Poll chunk `u0 / kChunk` of the band above until every word of it is
+// written; leaves it in the chunk buffer.  `v` holds a load issued earlier
+// and is re-polled only while incomplete.
+template <int K>
+__device__ __forceinline__ void acquire_chunk(float4 v, const float* up_stream, int u0, int Umax, int lane,
+                                              int chunk) {
+    using G = Geom<K>;
+    const int nvalid = min(kChunk, Umax - u0) * K * 2;  // floats
+    const bool mine = lane < G::CH4 && 4 * lane < nvalid;
+    while (!__all_sync(kFull, chunk_complete<K>(v, u0, Umax, lane))) {
         __nanosleep(32);
         if (mine) v = ld_relaxed_v4(up_stream + size_t(u0) * K * 2 + 4 * lane);
     }
-    if (mine) reinterpret_cast<float4*>(chunk)[lane] = v;
+    if (mine) sts4(chunk + 4 * lane, v);
 }
 
 template <int K, bool V4>
-__device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int lane, float* sm, float eps,
+__device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int lane, unsigned sbase, float eps,
                                          float omega) {
     using Gm = Geom<K>;
     const int w = J.w, h = J.h;
     const int y0 = q * kBandRows;
     const int Umax = w + K - 1;
-    const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sm));
     const size_t slen = sweep_stream_len(w, K);
     const int sid = q * 3 + ch;  // stream index of this (band, channel)
     const float* up_stream = q > 0 ? J.stream + size_t(sid - 3) * slen : nullptr;
 
-    StepCtx cx;
-    cx.sm = sm;
-    cx.smw = sm;
+    StepCtx<K> cx;
+    cx.lb = lane * Gm::RS;
+    cx.ob = Gm::OFF_O + orow(lane) * Gm::OW;
     cx.lane = lane;
     cx.y0 = y0;
     cx.w = w;
@@ -353,8 +474,10 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     cx.has_down = q < J.nb - 1;
     cx.Umax = Umax;
     cx.my_stream = J.stream + size_t(sid) * slen;
-    cx.FO = J.fg_out + (long long)ch * J.ostride;
-    cx.BO = J.bg_out + (long long)ch * J.ostride;
+    // band-relative output base (row y0 - (K-1) may be -1.. for the first
+    // band: only the pointer arithmetic goes there, stores are bounds-checked)
+    cx.FO = J.fg_out + (long long)ch * J.ostride + (long long)(y0 - (K - 1)) * J.opitch;
+    cx.BO = J.bg_out + (long long)ch * J.ostride + (long long)(y0 - (K - 1)) * J.opitch;
     cx.opitch = J.opitch;
     cx.eps = eps;
     cx.omega = omega;
@@ -362,21 +485,25 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     // rows this lane streams
     const RowSrc own = make_rowsrc<K>(J, ch, y0, lane, true, true, true, sbase);
     const bool has_x = lane >= 32 - K || lane == 0;
-    const RowSrc ext = make_rowsrc<K>(J, ch, y0, lane == 0 ? 32 : lane - 32, has_x, lane >= 33 - K, lane == 0, sbase);
+    const RowSrc ext =
+        make_rowsrc<K>(J, ch, y0, lane == 0 ? 32 : lane - 32, has_x, lane >= 33 - K, lane == 0, sbase);
 
     LaneState<K> st;
 #pragma unroll
     for (int k = 0; k < K; ++k) st.outp[k] = st.rprev[k] = make_float2(0.0f, 0.0f);
 
-    // prologue: blocks below the first in-loop issue (t4 = -4 loads block
-    // (kLead - r) / 4 of row r)
-    for (int b = 0; b < ((Gm::kLead - own.r) >> 2); ++b) row_block<K, V4>(own, b, w);
-    if (has_x)
-        for (int b = 0; b < ((Gm::kLead - ext.r) >> 2); ++b) row_block<K, V4>(ext, b, w);
+    // prologue: the loads "issued before" the first group, then M-1 empty
+    // groups so that every group waits with the same cp.async.wait_group M-1
+    constexpr int t0 = -4;
+    prologue_row<K, V4>(own, t0, w);
+    if (has_x) prologue_row<K, V4>(ext, t0, w);
     cp_commit();
+#pragma unroll
+    for (int i = 1; i < Gm::M; ++i) cp_commit();
     // the band above's first chunk, polled when needed
     float4 pend = make_float4(0.f, 0.f, 0.f, 0.f);
     const bool lane_ch = lane < Gm::CH4;
+    bool pend_ok = false;  // pend holds the complete next chunk
     if (cx.has_up && lane_ch) pend = ld_relaxed_v4(up_stream + 4 * lane);
 
     // Border groups: bands touching row 0 or h-1, else the first and last ~32
@@ -384,34 +511,49 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     const bool yband = y0 - (K - 1) <= 0 || y0 + 31 >= h - 1;
     const int fast_lo = 32 + K, fast_hi = w - 2;  // a step tr is fast iff fast_lo <= tr < fast_hi
     const int tend = 31 + Umax;                   // lane 31's last column is Umax-1
-    for (int t4 = -4; t4 < tend; t4 += 4) {
-        row_block<K, V4>(own, (t4 + 4 + Gm::kLead - own.r) >> 2, w);
-        if (has_x) row_block<K, V4>(ext, (t4 + 4 + Gm::kLead - ext.r) >> 2, w);
-        cp_commit();
-        cp_wait<Gm::kLead / 4 - 1>();
-        if (t4 < 0) {
-            cp_wait<1>();  // the prologue group
-            __syncwarp();
-            const int aRow = Gm::OFF_A + (lane + K) * 32;
-#pragma unroll
-            for (int k = 0; k < K; ++k)  // coefficients of step 0
-                st.co[k] = slot_coef<K, true>(sm, aRow, (-lane + 1 - k - 1) & 31, k, -lane - k, y0 + lane - k, w, h,
-                                              eps, omega);
-            continue;
-        }
-        if (cx.has_up && (t4 % kChunk) == 0 && t4 < Umax) {
-            acquire_chunk<K>(pend, up_stream, t4, Umax, lane, sm + Gm::OFF_C);
-            if (t4 + kChunk < Umax && lane_ch)  // prefetch the next chunk
-                pend = ld_relaxed_v4(up_stream + size_t(t4 + kChunk) * K * 2 + 4 * lane);
-        }
+    // groups whose issued blocks are inside [0, w) for every row -K .. 32
+    const int issue_lo = 32 + 3 - 4 - Gm::L, issue_hi = w - 4 - 4 - Gm::L - K;
+    for (int t4 = t0; t4 < tend; t4 += 4) {
+        cp_wait<Gm::M - 1>();
         __syncwarp();
-        if (!yband && t4 >= fast_lo && t4 + 4 <= fast_hi) {
+        if (t4 < 0) {
+            // coefficients of step 0 (computed "at step -1")
+            const int rc = cx.lb + ((-1 - lane - Gm::SH) & (Gm::RW - 1));
 #pragma unroll
-            for (int s = 0; s < 4; ++s) band_step<K, false>(st, cx, t4 + s);
+            for (int k = 0; k < K; ++k) st.co[k] = first_coef<K>(rc, k, -lane - k, y0 + lane - k, w, h, eps, omega);
         } else {
+            if (cx.has_up && t4 < Umax) {
+                const int nxt = (t4 & ~(kChunk - 1)) + kChunk;  // the next chunk's first column
+                if ((t4 % kChunk) == 0) {
+                    acquire_chunk<K>(pend, up_stream, t4, Umax, lane, Gm::OFF_C);
+                    pend_ok = false;
+                    if (nxt < Umax && lane_ch)  // prefetch the next chunk
+                        pend = ld_relaxed_v4(up_stream + size_t(nxt) * K * 2 + 4 * lane);
+                } else if (!pend_ok && nxt < Umax) {
+                    // the prefetch found the next chunk incomplete: re-poll it
+                    // now rather than a full round trip when it is needed
+                    pend_ok = __all_sync(kFull, chunk_complete<K>(pend, nxt, Umax, lane));
+                    if (!pend_ok && lane_ch) pend = ld_relaxed_v4(up_stream + size_t(nxt) * K * 2 + 4 * lane);
+                }
+            }
+            __syncwarp();
+            if (!yband && t4 >= fast_lo && t4 + 4 <= fast_hi) {
+#pragma unroll
+                for (int s = 0; s < 4; ++s) band_step<K, false>(st, cx, t4 + s);
+            } else {
 #pragma unroll 1
-            for (int s = 0; s < 4; ++s) band_step<K, true>(st, cx, t4 + s);
+                for (int s = 0; s < 4; ++s) band_step<K, true>(st, cx, t4 + s);
+            }
         }
+        __syncwarp();  // every lane is done with the ring slots the next loads overwrite
+        if (V4 && !yband && t4 >= issue_lo && t4 < issue_hi) {
+            issue_row_fast<K, 15u>(own, t4);
+            issue_row_fast<K, 0u>(ext, t4);
+        } else {
+            issue_row<K, V4>(own, t4, w);
+            if (has_x) issue_row<K, V4>(ext, t4, w);
+        }
+        cp_commit();
     }
     cp_wait<0>();
     __syncwarp();
@@ -420,8 +562,7 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
 template <int K, bool V4>
 __global__ void __launch_bounds__(32) sweep_kernel(const SweepJob* __restrict__ jobs, const int2* __restrict__ order,
                                                     int total_items, unsigned* ticket, float eps, float omega) {
-    extern __shared__ float4 sm4[];
-    float* sm = reinterpret_cast<float*>(sm4);
+    const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sweep_sm4));
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned tk = 0;
@@ -431,9 +572,9 @@ __global__ void __launch_bounds__(32) sweep_kernel(const SweepJob* __restrict__ 
         const int2 jb = order[tk];  // (job, band * 3 + channel)
         const SweepJob J = jobs[jb.x];
         if (V4 && !J.vec4) {
-            run_band<K, false>(J, jb.y / 3, jb.y % 3, lane, sm, eps, omega);
+            run_band<K, false>(J, jb.y / 3, jb.y % 3, lane, sbase, eps, omega);
         } else {
-            run_band<K, V4>(J, jb.y / 3, jb.y % 3, lane, sm, eps, omega);
+            run_band<K, V4>(J, jb.y / 3, jb.y % 3, lane, sbase, eps, omega);
         }
     }
 }
