@@ -51,30 +51,54 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi sampling of SM clocks and throttle reasons during the timed
-    region (B200_PROFILING.md clocks line)."""
+    """SM clocks and throttle reasons sampled during the timed region
+    (B200_PROFILING.md clocks line): NVML every 20 ms, else nvidia-smi."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits: sw_power_cap, hw_slowdown, sw_thermal, hw_thermal
+    BITS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+            ("sw_power_cap", 0x4))
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
         self.samples = []
         self.stop = threading.Event()
         self.t = threading.Thread(target=self.run, daemon=True)
+        self.nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(gpu_index))
+        except Exception:
+            self.nvml = None
+
+    def sample_nvml(self):
+        nv, h = self.nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.samples.append([str(sm), str(mx), ""] + ["Active" if r & b else "Not Active" for _, b in self.BITS])
 
     def run(self):
         while not self.stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                if self.nvml:
+                    self.sample_nvml()
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self.stop.wait(0.2)
+            self.stop.wait(0.02 if self.nvml else 0.2)
 
     def __enter__(self):
         self.t.start()
@@ -235,7 +259,9 @@ def run_ours(args, rank, world, local):
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
-    launches = int(sum(v["launches"] for v in stats.values()) // max(args.steps, 1))
+    # profiled kernels (sweep, resample/upsample, coarse) plus one sentinel
+    # fill per sweep launch
+    launches = int((sum(v["launches"] for v in stats.values()) + stats["sweep"]["launches"]) // max(args.steps, 1))
 
     # ---- CPU baseline: the unmodified reference on this host (rank 0, N=1)
     cpu = None

@@ -82,7 +82,10 @@ inline size_t sweep_stream_floats(int w, int h, int K) {
 // Launch helpers (kernels.cu).  `jobs_dev` are device copies of the arrays.
 // Tiles of 128 x 8 destination pixels; total_tiles = sum over jobs.
 int resample_tiles(int dw, int dh);
-cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s);
+// blocks_per_sm: persistent grid size (16 fills the GPU; the side-stream
+// pyramid uses fewer so the main stream's kernels can co-reside)
+cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s,
+                            int blocks_per_sm = 16);
 // F/B upsample (sw <= dw, sh <= dh, six planes): shared-memory staged tiles
 int upsample_tiles(int dw, int dh);
 cudaError_t launch_upsample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s);

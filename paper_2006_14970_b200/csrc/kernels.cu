@@ -282,9 +282,16 @@ bool upsample_ok(int sw, int sh, int dw, int dh) {
 
 int resample_tiles(int dw, int dh) { return ((dw + kResCols - 1) / kResCols) * ((dh + kResRows - 1) / kResRows); }
 
-cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s) {
+cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s,
+                            int blocks_per_sm) {
     if (njobs <= 0 || total_tiles <= 0) return cudaSuccess;
-    const int gx = int(std::min<long long>(total_tiles, 148 * 16));
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int gx = int(std::min<long long>(total_tiles, (long long)sms * blocks_per_sm));
     resample_kernel<<<gx, kResCols, 0, s>>>(jobs_dev, njobs, int(total_tiles));
     return cudaGetLastError();
 }

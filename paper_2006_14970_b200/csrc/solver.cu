@@ -236,6 +236,8 @@ struct Plan {
     int nc = 0;                      // number of coarse levels (K4)
     size_t max_sub = 0;              // max pixels over levels < n-1
     size_t max_lvl = 0;              // max pixels over all levels
+    std::vector<size_t> ia_off;      // per level: float offset of its I/alpha block in lvlIA
+    size_t ia_floats = 0;            // all big sub-top levels' I/alpha (4 pitched planes each)
     bool multipass = false;
     size_t stream_floats = 0;        // per pass, max over big levels
     int max_bands = 0;
@@ -250,10 +252,15 @@ void plan_image(Plan& P, const fgm_params* p) {
     while (P.nc < n && P.nc < kMaxCoarseLevels && size_t(P.lv[size_t(P.nc)].w) * P.lv[size_t(P.nc)].h <= size_t(kCoarseCap))
         ++P.nc;
     if (P.nc == 0) throw RuntimeError("internal: first level exceeds the coarse capacity");
+    P.ia_off.assign(size_t(n), 0);
     for (int l = 0; l < n; ++l) {
         const size_t px = size_t(level_pitch(P.lv[size_t(l)].w)) * P.lv[size_t(l)].h;
         P.max_lvl = std::max(P.max_lvl, px);
         if (l < n - 1) P.max_sub = std::max(P.max_sub, px);
+        if (l >= P.nc && l < n - 1) {  // every level's I/alpha is resampled up front
+            P.ia_off[size_t(l)] = P.ia_floats;
+            P.ia_floats += (4 * px + 63) / 64 * 64;
+        }
         if (l >= P.nc) {
             for (int K : passes_for(P.lv[size_t(l)].iters)) {
                 P.stream_floats = std::max(P.stream_floats,
@@ -269,7 +276,7 @@ void plan_image(Plan& P, const fgm_params* p) {
 size_t plan_bytes(const Plan& P) {
     if (P.nc == int(P.lv.size())) return 0;
     size_t b = 0;
-    b += al(4 * P.max_sub * sizeof(float));                       // lvlIA
+    b += al(std::max<size_t>(P.ia_floats, 1) * sizeof(float));   // lvlIA (all levels)
     b += al(6 * P.max_lvl * sizeof(float));                       // fbInit
     if (P.multipass) b += al(6 * P.max_lvl * sizeof(float));      // fbTmp
     b += al(6 * std::max<size_t>(P.max_sub, 1) * sizeof(float));  // fbOut
@@ -279,7 +286,7 @@ size_t plan_bytes(const Plan& P) {
 
 void carve(Plan& P, Arena& A) {
     if (P.nc == int(P.lv.size())) return;
-    P.lvlIA = A.take<float>(4 * P.max_sub);
+    P.lvlIA = A.take<float>(std::max<size_t>(P.ia_floats, 1));
     P.fbInit = A.take<float>(6 * P.max_lvl);
     if (P.multipass) P.fbTmp = A.take<float>(6 * P.max_lvl);
     P.fbOut = A.take<float>(6 * std::max<size_t>(P.max_sub, 1));
@@ -376,7 +383,44 @@ struct LaunchRec {
     double bytes;
     void* dst = nullptr;
     const void* src = nullptr;
+    int side = 0;   // 1: runs on the side stream, then records event `ev`
+    int ev = -1;    // side: event to record after; main: event to wait for before
 };
+
+// The side stream of the calling thread's device (I/alpha pyramid, which
+// depends only on the inputs and overlaps the main stream's coarse levels,
+// upsamples and sweeps), and a pool of events.
+struct SideStream {
+    int dev = -1;
+    cudaStream_t s = nullptr;
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t event(size_t i) {
+        while (ev.size() <= i) {
+            cudaEvent_t e;
+            ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            ev.push_back(e);
+        }
+        return ev[i];
+    }
+};
+thread_local SideStream g_side;
+#ifndef FGM_SIDE_BLOCKS
+#define FGM_SIDE_BLOCKS 16
+#endif
+constexpr int kSideBlocksPerSM = FGM_SIDE_BLOCKS;
+
+SideStream& side_stream() {
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    if (g_side.dev != dev) {  // (a thread that switches devices re-creates it; the old one leaks)
+        g_side = SideStream{};
+        int lo = 0, hi = 0;  // lowest priority: its blocks yield SM slots to the main stream's
+        ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
+        ck(cudaStreamCreateWithPriority(&g_side.s, cudaStreamNonBlocking, lo), "cudaStreamCreate");
+        g_side.dev = dev;
+    }
+    return g_side;
+}
 
 void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s) {
     validate(p);
@@ -440,6 +484,39 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
         launches.push_back({kCoarse, 0, int(cj.size()), 0, false, st.push(cj), 0, 0, 0, bytes});
     }
 
+    // ---- I/alpha pyramid of every big sub-top level, on the side stream ----
+    // (step j's launch records event j; step j's sweep waits for it)
+    for (int j = 0; j < J; ++j) {
+        std::vector<ResampleJob> rj;
+        long long tiles = 0;
+        double rbytes = 0;
+        for (auto& P : plans) {
+            const int n = int(P.lv.size());
+            const int l = n - J + j;
+            if (l < P.nc || l >= n - 1) continue;
+            const Level L = P.lv[size_t(l)];
+            const long long px = (long long)L.w * L.h, fpx = (long long)P.io.W * P.io.H;
+            const int pp = level_pitch(L.w);
+            const long long pps = (long long)pp * L.h;
+            float* ia = P.lvlIA + P.ia_off[size_t(l)];
+            rj.push_back(rjob(P.io.img, ia, P.io.W, P.io.H, L.w, L.h, 3, P.io.W, pp));
+            rj.push_back(rjob(P.io.alpha, ia + 3 * pps, P.io.W, P.io.H, L.w, L.h, 1, P.io.W, pp));
+            rbytes += 4.0 * 4 * (double(px) + std::min<double>(double(fpx), 4.0 * px));
+        }
+        if (rj.empty()) continue;
+        for (auto& r : rj) {
+            r.tile_base = int(tiles);
+            tiles += resample_tiles(r.dw, r.dh);
+        }
+        LaunchRec lr{kResample, 0, int(rj.size()), 0, false, st.push(rj), 0, 0, tiles, rbytes};
+        lr.side = 1;
+        lr.ev = j;
+        launches.push_back(lr);
+    }
+    std::vector<char> has_ia(size_t(J), 0);
+    for (const auto& r : launches)
+        if (r.side) has_ia[size_t(r.ev)] = 1;
+
     // ---- big levels, aligned so that every image's top level is step J-1 --
     for (int j = 0; j < J; ++j) {
         std::vector<ResampleJob> rj, uj;  // resample (I/alpha) and upsample (F/B) jobs
@@ -457,14 +534,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             act.push_back({&P, l});
             const Level L = P.lv[size_t(l)], Lp = P.lv[size_t(l - 1)];
             const long long px = (long long)L.w * L.h, ppx = (long long)Lp.w * Lp.h;
-            const long long fpx = (long long)P.io.W * P.io.H;
             const int pp = level_pitch(L.w);
-            const long long pps = (long long)pp * L.h;  // pitched plane of this level
-            if (l < n - 1) {
-                rj.push_back(rjob(P.io.img, P.lvlIA, P.io.W, P.io.H, L.w, L.h, 3, P.io.W, pp));
-                rj.push_back(rjob(P.io.alpha, P.lvlIA + 3 * pps, P.io.W, P.io.H, L.w, L.h, 1, P.io.W, pp));
-                rbytes += 4.0 * 4 * (double(px) + std::min<double>(double(fpx), 4.0 * px));
-            }
             // the previous level's output: the coarse kernel's or a sweep's (both
             // pitched); levels grow, so this is an upsample (staged kernel)
             const ResampleJob fj = rjob(P.fbOut, P.fbInit, Lp.w, Lp.h, L.w, L.h, 6, level_pitch(Lp.w), pp);
@@ -514,8 +584,9 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                     SweepJob J1{};
                     // the top level reads/writes the caller's dense planes, the
                     // others the solver's pitched level buffers
-                    J1.img = top ? P.io.img : P.lvlIA;
-                    J1.alpha = top ? P.io.alpha : P.lvlIA + 3 * pps;
+                    float* ia = P.lvlIA + P.ia_off[size_t(a.l)];
+                    J1.img = top ? P.io.img : ia;
+                    J1.alpha = top ? P.io.alpha : ia + 3 * pps;
                     J1.ipitch = top ? L.w : pp;
                     J1.istride = top ? px : pps;
                     J1.fg_in = in;
@@ -551,8 +622,10 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 const bool full = use_full_kernel(total, K);
                 const size_t off = st.push(sj);
                 const size_t ooff = st.push(band_order(sj, full));
-                launches.push_back({kSweep, K, int(sj.size()), full ? total : 3 * total, full, off, ticket, ooff,
-                                    (long long)max_stream, sbytes});
+                LaunchRec lr{kSweep, K, int(sj.size()), full ? total : 3 * total, full, off, ticket, ooff,
+                             (long long)max_stream, sbytes};
+                if (pi == 0 && has_ia[size_t(j)]) lr.ev = j;  // this step's I/alpha pyramid level
+                launches.push_back(lr);
             }
         }
         for (auto& a : act) {  // per-level dumps (debug API)
@@ -578,7 +651,28 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
     ck(cudaMemsetAsync(dctr, 0, std::max<size_t>(st.counters, 1) * sizeof(unsigned), s), "cudaMemsetAsync");
     g_pinned.stage(st.host.data(), st.host.size(), s, djobs);
 
-    for (const LaunchRec& r : launches) {
+    // the side stream starts after everything enqueued on s so far (inputs,
+    // job uploads) and s waits for all of its work at the end
+    SideStream& side = side_stream();
+    const cudaEvent_t ev_start = side.event(size_t(J)), ev_end = side.event(size_t(J) + 1);
+    bool any_side = false;
+    for (const LaunchRec& r : launches) any_side = any_side || r.side;
+    if (any_side) {
+        ck(cudaEventRecord(ev_start, s), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(side.s, ev_start, 0), "cudaStreamWaitEvent");
+    }
+
+    for (const LaunchRec& r0 : launches) {
+        const LaunchRec& r = r0;
+        if (r.side) {  // I/alpha pyramid level
+            ProfScope ps(side.s, 1, r.bytes);
+            ck(launch_resample(reinterpret_cast<const ResampleJob*>(djobs + r.job_off), r.njobs, r.max_rows, side.s,
+                               kSideBlocksPerSM),
+               "resample_kernel");
+            ck(cudaEventRecord(side.event(size_t(r.ev)), side.s), "cudaEventRecord");
+            continue;
+        }
+        if (r.ev >= 0) ck(cudaStreamWaitEvent(s, side.event(size_t(r.ev)), 0), "cudaStreamWaitEvent");
         switch (r.kind) {
             case kCoarse: {
                 ProfScope ps(s, 2, r.bytes);
@@ -620,6 +714,10 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                    "cudaMemcpy2DAsync");
                 break;
         }
+    }
+    if (any_side) {  // nothing of this call stays outstanding on the side stream
+        ck(cudaEventRecord(ev_end, side.s), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(s, ev_end, 0), "cudaStreamWaitEvent");
     }
 }
 
@@ -762,11 +860,14 @@ int fgm_batch_solve_host_f32(int n_images, const float* const* images, const flo
         for (int i = 0; i < n_images; ++i) check_dims(widths[i], heights[i]);
         if (n_images == 0) return;
         require_device();
-        // Sub-batches of ~1/8 of the pixels (at least one image each): copy-in
-        // of group g+1 and copy-out of group g-1 overlap the solve of group g.
+        // Sub-batches of ~1/16 of the pixels (at least one image each) in
+        // kSlots device slots: copy-in runs up to kSlots groups ahead of
+        // copy-out, so both PCIe directions stay busy while the (much
+        // shorter) solves run in between.
+        constexpr size_t kGroups = 16, kSlots = 4;
         size_t total = 0;
         for (int i = 0; i < n_images; ++i) total += size_t(widths[i]) * heights[i];
-        const size_t target = std::max<size_t>(total / 8, 1);
+        const size_t target = std::max<size_t>(total / kGroups, 1);
         std::vector<std::pair<int, int>> groups;  // [begin, end)
         for (int b = 0; b < n_images;) {
             int e = b;
@@ -790,7 +891,7 @@ int fgm_batch_solve_host_f32(int n_images, const float* const* images, const flo
                 cudaStreamDestroy(c);
             }
         } sg{sc, sin, sout};
-        // two device slots of the largest group, 10 floats per pixel each
+        // kSlots device slots of the largest group, 10 floats per pixel each
         size_t gmax = 0;
         for (auto [b, e] : groups) {
             size_t px = 0;
@@ -799,7 +900,9 @@ int fgm_batch_solve_host_f32(int n_images, const float* const* images, const flo
         }
         const size_t slot_floats = 10 * gmax + 64 * size_t(n_images);
         float* dbuf = nullptr;
-        ck(cudaMallocAsync(reinterpret_cast<void**>(&dbuf), 2 * slot_floats * sizeof(float), sc), "cudaMallocAsync");
+        const size_t nslots = std::min(kSlots, groups.size());
+        ck(cudaMallocAsync(reinterpret_cast<void**>(&dbuf), nslots * slot_floats * sizeof(float), sc),
+           "cudaMallocAsync");
         std::vector<cudaEvent_t> ev_in(groups.size()), ev_done(groups.size()), ev_out(groups.size());
         for (size_t g = 0; g < groups.size(); ++g) {
             ck(cudaEventCreateWithFlags(&ev_in[g], cudaEventDisableTiming), "cudaEventCreate");
@@ -809,9 +912,9 @@ int fgm_batch_solve_host_f32(int n_images, const float* const* images, const flo
         ck(cudaStreamSynchronize(sc), "cudaStreamSynchronize");
         for (size_t g = 0; g < groups.size(); ++g) {
             const auto [b, e] = groups[g];
-            float* slot = dbuf + (g & 1) * slot_floats;
-            // the slot's previous user (group g-2) must have been copied out
-            if (g >= 2) ck(cudaStreamWaitEvent(sin, ev_out[g - 2], 0), "cudaStreamWaitEvent");
+            float* slot = dbuf + (g % nslots) * slot_floats;
+            // the slot's previous user (group g - nslots) must have been copied out
+            if (g >= nslots) ck(cudaStreamWaitEvent(sin, ev_out[g - nslots], 0), "cudaStreamWaitEvent");
             std::vector<ImageIO> io;
             size_t off = 0;
             for (int i = b; i < e; ++i) {
@@ -874,7 +977,10 @@ int fgm_resize_f32(const float* src, int sw, int sh, int nplanes, float* dst, in
         rj.tile_base = 0;
         ResampleJob* d = A.take<ResampleJob>(1);
         ck(cudaMemcpyAsync(d, &rj, sizeof(rj), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
-        ck(launch_resample(d, 1, resample_tiles(dw, dh), s), "resample_kernel");
+        if (nplanes == 6 && upsample_ok(sw, sh, dw, dh))  // the solver's F/B upsample path
+            ck(launch_upsample(d, 1, upsample_tiles(dw, dh), s), "upsample_kernel");
+        else
+            ck(launch_resample(d, 1, resample_tiles(dw, dh), s), "resample_kernel");
     });
 }
 

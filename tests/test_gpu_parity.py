@@ -152,6 +152,24 @@ def test_resize_vs_reference_fixture(fgm, cuda):
         assert np.abs(out - z[key]).max() < 1e-6
 
 
+@pytest.mark.parametrize("sw,sh,dw,dh", [(32, 28, 64, 55), (395, 274, 768, 512), (790, 563, 1539, 1062),
+                                         (1539, 1062, 3000, 2000), (7, 6, 14, 12), (100, 3, 161, 5),
+                                         (13, 9, 40, 33), (333, 517, 600, 830)])
+def test_upsample_six_planes(fgm, cuda, orc, sw, sh, dw, dh):
+    # six planes at scale <= 0.625 take the staged F/B upsample kernel (the
+    # solver's level-to-level path): bitwise equal to the generic resample
+    # kernel (one plane at a time), and to the fp32 oracle resize within the
+    # FMA-contraction rounding (the oracle is built with -ffp-contract=off)
+    rng = np.random.default_rng(sw * 7 + dh)
+    src = rng.random((6, sh, sw), dtype=np.float32)
+    x = dev(src, cuda)
+    out = fgm.resize_cuda(x, dw, dh)
+    planes = torch.cat([fgm.resize_cuda(x[p:p + 1].contiguous(), dw, dh) for p in range(6)])
+    assert torch.equal(out, planes)
+    ref = orc.resize(src, dw, dh)
+    assert np.abs(out.cpu().numpy() - ref).max() <= 2e-7
+
+
 def test_resize_identity_and_errors(fgm, cuda):
     x = torch.rand(3, 6, 9, device=cuda)
     assert torch.equal(fgm.resize_cuda(x, 9, 6), x)
