@@ -559,8 +559,11 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     __syncwarp();
 }
 
+#ifndef FGM_SWEEP_MINB
+#define FGM_SWEEP_MINB 1
+#endif
 template <int K, bool V4>
-__global__ void __launch_bounds__(32) sweep_kernel(const SweepJob* __restrict__ jobs, const int2* __restrict__ order,
+__global__ void __launch_bounds__(32, FGM_SWEEP_MINB) sweep_kernel(const SweepJob* __restrict__ jobs, const int2* __restrict__ order,
                                                     int total_items, unsigned* ticket, float eps, float omega) {
     const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sweep_sm4));
     const int lane = threadIdx.x & 31;
