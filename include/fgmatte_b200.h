@@ -18,6 +18,10 @@
  *   fgm_batch_solve_f32      <- N independent ml_foreground_background calls
  *                               (the reference is reentrant)
  *   fgm_resize_f32           <- fgmatte::resize              src/image.cpp:114-133
+ *   fgm_ml_solve_hwc         <- _fgmatte.ml_foreground_background with its
+ *                               HWC conversion loops     python/bindings.cpp:20-53,146-157
+ *   fgm_compose_f32          <- fgmatte::compose             src/image.cpp:39-57
+ *                               (python/bindings.cpp:89-95)
  *   fgm_sweep_passes_f32     <- `iterations` x sweep         src/multilevel.cpp:81-121, 162-163
  *
  * Conventions: planar fp32 (plane(c)[y*w + x], as image.hpp:22-26), image = 3
@@ -95,6 +99,20 @@ int fgm_batch_solve_host_f32(int n_images, const float* const* images, const flo
 /* Bilinear, centre-aligned, edge-clamped resize of `nplanes` planes with
  * clamp01, identity copy at equal size (image.cpp:71-133).  Device pointers. */
 int fgm_resize_f32(const float* src, int sw, int sh, int nplanes, float* dst, int dw, int dh, void* stream);
+
+/* The Python binding's boundary on the device (bindings.cpp:20-53, 146-157):
+ * interleaved (h, w, 3) image and (h, w) alpha of float (f64 = 0) or double
+ * (f64 = 1), clamped to [0, 1] on the way in as the binding does, solved, and
+ * written back interleaved in the same type.  Device pointers, enqueued on
+ * `stream` (zero-copy for torch / DLPack callers). */
+int fgm_ml_solve_hwc(const void* image_hwc, const void* alpha, int w, int h, int f64, const fgm_params* p,
+                     void* fg_hwc, void* bg_hwc, void* stream);
+
+/* Composite: out_c = clamp01(alpha * fg_c + (1 - alpha) * bg_c) for `nch`
+ * planes (image.cpp:39-57); the epilogue that puts an estimated foreground on
+ * a new background.  Device pointers; out may alias fg or bg. */
+int fgm_compose_f32(const float* fg, const float* bg, const float* alpha, int w, int h, int nch, float* out,
+                    void* stream);
 
 /* `iterations` exact Gauss-Seidel scanline sweeps of one level, given the
  * level's image/alpha and initial F/B (device pointers; fg_out/bg_out may not

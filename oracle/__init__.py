@@ -84,6 +84,8 @@ class _Oracle:
                                        C.c_int, _dp, _dp]
         L.fgmo_resize_f64.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, C.c_int, C.c_int]
         L.fgmo_resize_f32.argtypes = [_fp, C.c_int, C.c_int, C.c_int, _fp, C.c_int, C.c_int]
+        L.fgmo_compose_f64.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, C.c_int, _dp]
+        L.fgmo_compose_f32.argtypes = [_fp, _fp, _fp, C.c_int, C.c_int, C.c_int, _fp]
         L.fgmo_sweep_f64.argtypes = [_dp, _dp, _dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double]
         L.fgmo_sweep_f32.argtypes = [_fp, _fp, _fp, _fp, C.c_int, C.c_int, C.c_double, C.c_double]
         L.fgmo_ml_solve_f64.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
@@ -105,6 +107,19 @@ class _Oracle:
         t = (C.c_double * dst)()
         self.lib.fgmo_make_taps(src, dst, i0, i1, t)
         return np.array(i0[:]), np.array(i1[:]), np.array(t[:])
+
+    def compose(self, fg, bg, alpha):
+        """image.cpp:39-57.  fg, bg: (C, H, W); alpha: (H, W).  fp64 or fp32."""
+        nch, h, w = fg.shape
+        if fg.dtype == np.float32:
+            f, b, a = _f32(fg), _f32(bg), _f32(alpha)
+            out = np.empty((nch, h, w), np.float32)
+            self.lib.fgmo_compose_f32(_ptr(f, _fp), _ptr(b, _fp), _ptr(a, _fp), w, h, nch, _ptr(out, _fp))
+        else:
+            f, b, a = _f64(fg), _f64(bg), _f64(alpha)
+            out = np.empty((nch, h, w))
+            self.lib.fgmo_compose_f64(_ptr(f, _dp), _ptr(b, _dp), _ptr(a, _dp), w, h, nch, _ptr(out, _dp))
+        return out
 
     def resize(self, src, dw, dh):
         """src: (C, H, W) or (H, W).  fp64 -> fp64, fp32 -> fp32."""
@@ -189,6 +204,7 @@ class _Reference:
         L.fgmr_level_schedule.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
                                           _ip, _ip, _ip, C.c_int]
         L.fgmr_resize.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, C.c_int, C.c_int]
+        L.fgmr_compose.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, C.c_int, _dp]
         L.fgmr_solve_pixel.argtypes = [C.c_double, _dp, C.c_int, _dp, _dp, _dp, C.c_double, C.c_double, C.c_int,
                                        _dp, _dp]
         L.fgmr_ml_solve.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
@@ -218,6 +234,13 @@ class _Reference:
         out = np.empty((nch, dh, dw))
         self._check(self.lib.fgmr_resize(_ptr(s, _dp), sw, sh, nch, _ptr(out, _dp), dw, dh))
         return out[0] if two_d else out
+
+    def compose(self, fg, bg, alpha):
+        nch, h, w = fg.shape
+        f, b, a = _f64(fg), _f64(bg), _f64(alpha)
+        out = np.empty((nch, h, w))
+        self._check(self.lib.fgmr_compose(_ptr(f, _dp), _ptr(b, _dp), _ptr(a, _dp), w, h, nch, _ptr(out, _dp)))
+        return out
 
     def solve_pixel(self, alpha_i, intensity, nalpha, nfg, nbg, omega=0.1, eps_r=5e-3, clamp=True):
         n = len(nalpha)

@@ -21,6 +21,9 @@ int fgmo_ml_solve_f64(const double* image, const double* alpha, int w, int h, do
                       int low_res_threshold, int iters_low, int iters_high, double* fg, double* bg,
                       double** level_fg, double** level_bg);
 
+void fgmo_compose_f64(const double* fg, const double* bg, const double* alpha, int w, int h, int nch, double* out);
+void fgmo_compose_f32(const float* fg, const float* bg, const float* alpha, int w, int h, int nch, float* out);
+
 void fgmo_resize_f32(const float* src, int sw, int sh, int nch, float* dst, int dw, int dh);
 void fgmo_sweep_f32(const float* image, const float* alpha, float* fg, float* bg, int w, int h, double omega,
                     double eps_r);

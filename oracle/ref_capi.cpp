@@ -87,6 +87,20 @@ int fgmr_resize(const double* src, int sw, int sh, int nch, double* dst, int dw,
     });
 }
 
+// fgmatte::compose, image.cpp:39-57 (planar fg/bg with nch channels, alpha w*h)
+int fgmr_compose(const double* fg, const double* bg, const double* alpha, int w, int h, int nch, double* out) {
+    return run_guarded([&] {
+        const size_t n = size_t(w) * h;
+        Image f(w, h, nch), b(w, h, nch);
+        AlphaMatte a(w, h);
+        std::memcpy(f.data().data(), fg, sizeof(double) * n * size_t(nch));
+        std::memcpy(b.data().data(), bg, sizeof(double) * n * size_t(nch));
+        std::memcpy(a.data().data(), alpha, sizeof(double) * n);
+        const Image o = compose(f, b, a);
+        std::memcpy(out, o.data().data(), sizeof(double) * n * size_t(nch));
+    });
+}
+
 // fgmatte::solve_pixel / solve_pixel_raw, multilevel.cpp:125-139
 int fgmr_solve_pixel(double alpha_i, const double* intensity, int n, const double* nalpha, const double* nfg,
                      const double* nbg, double omega, double eps_r, int clamp, double* fg_out, double* bg_out) {

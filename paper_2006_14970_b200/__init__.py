@@ -65,6 +65,11 @@ class Params:
     iters_low: int = 10
     iters_high: int = 2
 
+    def kwargs(self) -> dict:
+        """Keyword arguments of ml_foreground_background."""
+        return {"omega": self.omega, "eps_r": self.eps_r, "low_res_threshold": self.low_res_threshold,
+                "iters_low": self.iters_low, "iters_high": self.iters_high}
+
     def c(self) -> _CParams:
         return _CParams(float(self.eps_r), float(self.omega), int(self.iters_low), int(self.iters_high),
                         int(self.low_res_threshold))
@@ -104,6 +109,8 @@ def _load():
     L.fgm_batch_solve_host_f32.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(vp), ip, ip, P, C.POINTER(vp),
                                            C.POINTER(vp)]
     L.fgm_resize_f32.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp]
+    L.fgm_compose_f32.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp]
+    L.fgm_ml_solve_hwc.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, P, vp, vp, vp]
     L.fgm_sweep_passes_f32.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp, vp,
                                        vp]
     L.fgm_profile_enable.argtypes = [C.c_int]
@@ -176,7 +183,15 @@ def _alpha_from_array(arr) -> np.ndarray:
 def ml_foreground_background(image, alpha, omega: float = 0.1, eps_r: float = 5e-3, low_res_threshold: int = 32,
                              iters_low: int = 10, iters_high: int = 2):
     """Multi-level foreground/background colour estimation; returns (fg, bg)
-    as float64 HWC arrays (bindings.cpp:146-157).  Runs on the GPU."""
+    as float64 HWC arrays (bindings.cpp:146-157).  Runs on the GPU.
+
+    CUDA tensors (torch, or any object exporting ``__dlpack__`` on a CUDA
+    device) stay on the device: HWC float32/float64 in, the binding's clamp and
+    layout conversion done by a kernel, HWC tensors of the same dtype out."""
+    dev = _cuda_tensor(image)
+    if dev is not None:
+        return _ml_foreground_background_hwc_device(dev, _cuda_tensor(alpha, like=dev),
+                                                    Params(omega, eps_r, low_res_threshold, iters_low, iters_high))
     img = _image_from_array(image)
     a = _alpha_from_array(alpha)
     c, h, w = img.shape
@@ -193,6 +208,53 @@ def ml_foreground_background(image, alpha, omega: float = 0.1, eps_r: float = 5e
     _check(L.fgm_ml_solve_host_f64(img.ctypes.data_as(dp), a.ctypes.data_as(dp), w, h, C.byref(p),
                                    fg.ctypes.data_as(dp), bg.ctypes.data_as(dp)))
     return np.ascontiguousarray(fg.transpose(1, 2, 0)), np.ascontiguousarray(bg.transpose(1, 2, 0))
+
+
+def _cuda_tensor(x, like=None):
+    """x as a torch CUDA tensor (zero-copy through DLPack), or None for host data."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return None
+    if isinstance(x, torch.Tensor):
+        t = x
+    elif hasattr(x, "__dlpack__") and not isinstance(x, np.ndarray):
+        t = torch.from_dlpack(x)
+    else:
+        if like is not None:  # alpha given on the host next to a device image
+            return torch.as_tensor(np.asarray(x), device=like.device, dtype=like.dtype)
+        return None
+    if not t.is_cuda:
+        return None if like is None else t.to(like.device)
+    return t
+
+
+def _ml_foreground_background_hwc_device(image, alpha, params):
+    import torch
+
+    if image.dim() == 2:
+        image = image[..., None]
+    if image.dim() != 3:
+        raise ValueError("image array must have 2 or 3 dimensions")
+    h, w, c = image.shape
+    if c not in (1, 3):
+        raise ValueError("image must have 1 or 3 channels")
+    if c != 3:
+        raise ValueError(f"ml_foreground_background: image must have 3 channels, got {c}")
+    if alpha.dim() != 2:
+        raise ValueError("alpha array must have 2 dimensions")
+    if tuple(alpha.shape) != (h, w):
+        raise ValueError(f"ml_foreground_background: alpha size {alpha.shape[1]}x{alpha.shape[0]} does not match "
+                         f"image size {w}x{h}")
+    dt = torch.float64 if image.dtype == torch.float64 else torch.float32
+    image = image.to(dtype=dt).contiguous()
+    alpha = alpha.to(device=image.device, dtype=dt).contiguous()
+    fg = torch.empty((h, w, 3), device=image.device, dtype=dt)
+    bg = torch.empty_like(fg)
+    p = params.c()
+    _check(_load().fgm_ml_solve_hwc(image.data_ptr(), alpha.data_ptr(), w, h, 1 if dt == torch.float64 else 0,
+                                    C.byref(p), fg.data_ptr(), bg.data_ptr(), _stream_ptr(image.device)))
+    return fg, bg
 
 
 def resize(array, width: int, height: int):
@@ -337,6 +399,24 @@ def resize_cuda(src, width: int, height: int):
     out = torch.empty((src.shape[0], height, width), device=src.device, dtype=torch.float32)
     _check(_load().fgm_resize_f32(src.data_ptr(), src.shape[2], src.shape[1], src.shape[0], out.data_ptr(), width,
                                   height, _stream_ptr(src.device)))
+    return out
+
+
+def compose_cuda(fg, bg, alpha, out=None):
+    """Composite fg over bg (image.cpp:39-57; `_fgmatte.compose`, bindings.cpp:89-95):
+    (C, H, W) float32 CUDA tensors fg, bg and (H, W) alpha -> (C, H, W)."""
+    import torch
+
+    fg, bg, alpha = _dev_f32(fg, "fg"), _dev_f32(bg, "bg"), _dev_f32(alpha, "alpha")
+    if alpha.dim() == 3 and alpha.shape[0] == 1:
+        alpha = alpha[0]
+    if bg.shape != fg.shape:
+        raise ValueError(f"compose: bg size {tuple(bg.shape)} does not match fg size {tuple(fg.shape)}")
+    if tuple(alpha.shape) != tuple(fg.shape[1:]):
+        raise ValueError(f"compose: alpha size {tuple(alpha.shape)} does not match fg size {tuple(fg.shape[1:])}")
+    out = torch.empty_like(fg) if out is None else out
+    _check(_load().fgm_compose_f32(fg.data_ptr(), bg.data_ptr(), alpha.data_ptr(), fg.shape[2], fg.shape[1],
+                                   fg.shape[0], out.data_ptr(), _stream_ptr(fg.device)))
     return out
 
 

@@ -89,7 +89,11 @@ cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long to
 // F/B upsample (sw <= dw, sh <= dh, six planes): shared-memory staged tiles
 int upsample_tiles(int dw, int dh);
 cudaError_t launch_upsample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s);
-bool upsample_ok(int sw, int sh, int dw, int dh);  // scale within the staged window
+bool upsample_ok(int sw, int sh, int dw, int dh);
+cudaError_t launch_hwc_to_planar(const void* src, bool f64, long long n, int ch, float* dst, cudaStream_t s);
+cudaError_t launch_planar_to_hwc(const float* src, long long n, int ch, void* dst, bool f64, cudaStream_t s);
+cudaError_t launch_compose(const float* fg, const float* bg, const float* alpha, long long n, int nch, float* out,
+                           cudaStream_t s);  // scale within the staged window
 cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float omega, cudaStream_t s);
 // order_dev[t] = (job, 3 * band + channel) of ticket t, band-major across jobs.
 cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands, unsigned* ticket,

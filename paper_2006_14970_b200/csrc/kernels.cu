@@ -296,6 +296,67 @@ cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long to
     return cudaGetLastError();
 }
 
+// ----------------------------------------------------------------------------
+// K5 layout kernels of the HWC boundary (python/bindings.cpp:20-53): an
+// interleaved (h, w, ch) image of T (float or double) to planar fp32 with the
+// binding's clamp01 on every input value, and planar fp32 back to (h, w, 3).
+template <typename T>
+__global__ void hwc_to_planar_kernel(const T* __restrict__ src, long long n, int ch, float* __restrict__ dst) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+        for (int c = 0; c < ch; ++c) {
+            const double v = double(src[i * ch + c]);
+            dst[(long long)c * n + i] = float(v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v));  // clamp01 in the source type
+        }
+}
+
+template <typename T>
+__global__ void planar_to_hwc_kernel(const float* __restrict__ src, long long n, int ch, T* __restrict__ dst) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+        for (int c = 0; c < ch; ++c) dst[i * ch + c] = T(src[(long long)c * n + i]);
+}
+
+cudaError_t launch_hwc_to_planar(const void* src, bool f64, long long n, int ch, float* dst, cudaStream_t s) {
+    const int gx = std::max(1, int(std::min<long long>((n + 255) / 256, 148 * 16)));
+    if (f64)
+        hwc_to_planar_kernel<double><<<gx, 256, 0, s>>>(static_cast<const double*>(src), n, ch, dst);
+    else
+        hwc_to_planar_kernel<float><<<gx, 256, 0, s>>>(static_cast<const float*>(src), n, ch, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_planar_to_hwc(const float* src, long long n, int ch, void* dst, bool f64, cudaStream_t s) {
+    const int gx = std::max(1, int(std::min<long long>((n + 255) / 256, 148 * 16)));
+    if (f64)
+        planar_to_hwc_kernel<double><<<gx, 256, 0, s>>>(src, n, ch, static_cast<double*>(dst));
+    else
+        planar_to_hwc_kernel<float><<<gx, 256, 0, s>>>(src, n, ch, static_cast<float*>(dst));
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------
+// Compose epilogue (image.cpp:39-57): out = clamp01(a * f + (1 - a) * b) per
+// plane, in the reference's operation order (a*f, (1-a)*b, add; no FMA).
+__global__ void compose_kernel(const float* __restrict__ fg, const float* __restrict__ bg,
+                               const float* __restrict__ alpha, long long n, int nch, float* out) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float a = alpha[i], ia = __fsub_rn(1.0f, a);
+        for (int c = 0; c < nch; ++c) {
+            const long long j = (long long)c * n + i;
+            out[j] = __saturatef(__fadd_rn(__fmul_rn(a, fg[j]), __fmul_rn(ia, bg[j])));
+        }
+    }
+}
+
+cudaError_t launch_compose(const float* fg, const float* bg, const float* alpha, long long n, int nch, float* out,
+                           cudaStream_t s) {
+    const int gx = int(std::min<long long>((n + 255) / 256, 148 * 16));
+    compose_kernel<<<std::max(gx, 1), 256, 0, s>>>(fg, bg, alpha, n, nch, out);
+    return cudaGetLastError();
+}
+
 // ============================================================================
 // K4: coarse levels.  One CTA per image.  Per level: resample I/alpha from
 // full-res (global) and F/B from the previous level (shared), then

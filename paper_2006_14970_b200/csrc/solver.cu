@@ -984,6 +984,40 @@ int fgm_resize_f32(const float* src, int sw, int sh, int nplanes, float* dst, in
     });
 }
 
+int fgm_ml_solve_hwc(const void* image_hwc, const void* alpha, int w, int h, int f64, const fgm_params* p,
+                     void* fg_hwc, void* bg_hwc, void* stream) {
+    return guarded([&] {
+        check_dims(w, h);
+        validate(p);
+        if (!image_hwc || !alpha || !fg_hwc || !bg_hwc) throw InvalidArgument("ml_foreground_background: null buffer");
+        require_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t n = size_t(w) * h;
+        Arena A;
+        A.reserve(al(10 * n * sizeof(float)), s);
+        float* dimg = A.take<float>(4 * n);  // 3 image planes + alpha
+        float* dout = A.take<float>(6 * n);
+        ck(launch_hwc_to_planar(image_hwc, f64 != 0, (long long)n, 3, dimg, s), "hwc_to_planar");
+        ck(launch_hwc_to_planar(alpha, f64 != 0, (long long)n, 1, dimg + 3 * n, s), "hwc_to_planar");
+        std::vector<ImageIO> io{{dimg, dimg + 3 * n, w, h, dout, dout + 3 * n, nullptr, nullptr}};
+        solve_batch(io, p, s);
+        ck(launch_planar_to_hwc(dout, (long long)n, 3, fg_hwc, f64 != 0, s), "planar_to_hwc");
+        ck(launch_planar_to_hwc(dout + 3 * n, (long long)n, 3, bg_hwc, f64 != 0, s), "planar_to_hwc");
+    });
+}
+
+int fgm_compose_f32(const float* fg, const float* bg, const float* alpha, int w, int h, int nch, float* out,
+                    void* stream) {
+    return guarded([&] {
+        check_dims(w, h);
+        if (nch < 1) throw InvalidArgument("compose: channels must be >= 1, got " + std::to_string(nch));
+        if (!fg || !bg || !alpha || !out) throw InvalidArgument("compose: null buffer");
+        require_device();
+        ck(launch_compose(fg, bg, alpha, (long long)w * h, nch, out, static_cast<cudaStream_t>(stream)),
+           "compose_kernel");
+    });
+}
+
 int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg_in, const float* bg_in, int w,
                          int h, int iterations, double regularization, double gradient_weight, float* fg_out,
                          float* bg_out, void* stream) {

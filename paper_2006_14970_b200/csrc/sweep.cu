@@ -399,8 +399,8 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
             const int yf = y0 + jf - (K - 1);
             ok = xs >= 0 && xs + OW - 1 < w && yf >= 0 && yf < h;
         }
-        if (ok) {
-            const int off = jf * x_.opitch + xs + col;
+        if (ok) {  // off >= 0 here: unsigned, one IMAD.WIDE.U32 per plane
+            const unsigned off = unsigned(jf * x_.opitch + xs + col);
             const int o = Gm::OFF_O + orow(jf) * OW + col;
             stg(x_.FO + off, lds(o));
             stg(x_.BO + off, lds(o + Gm::OPL));
@@ -410,7 +410,7 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
             const int x0 = (w - 1) & ~(OW - 1);
             const int ye = y0 + je - (K - 1);
             if (je >= 0 && je < 32 && ye >= 0 && ye < h && lane < w - x0) {
-                const int off = je * x_.opitch + x0 + lane;
+                const unsigned off = unsigned(je * x_.opitch + x0 + lane);
                 const int o = Gm::OFF_O + orow(je) * OW + lane;
                 stg(x_.FO + off, lds(o));
                 stg(x_.BO + off, lds(o + Gm::OPL));

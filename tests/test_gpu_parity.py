@@ -170,6 +170,47 @@ def test_upsample_six_planes(fgm, cuda, orc, sw, sh, dw, dh):
     assert np.abs(out.cpu().numpy() - ref).max() <= 2e-7
 
 
+# ---- device HWC boundary of the Python entry point ----
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_ml_foreground_background_device_hwc(fgm, cuda, dtype):
+    from paper_2006_14970_b200 import synth
+    img, alpha = synth.make_composite(97, 61, synth.BASE_SEED + 8, ellipses=3, edge=3.0)
+    hwc = img.permute(1, 2, 0).contiguous().numpy().astype(dtype)
+    a = alpha.numpy().astype(dtype)
+    a[0, :5] = 1.3  # out-of-range inputs are clamped like the binding (bindings.cpp:36, 62)
+    f_host, b_host = fgm.ml_foreground_background(hwc, a, **fgm.BASELINE_PARAMS.kwargs())
+    f_dev, b_dev = fgm.ml_foreground_background(torch.from_numpy(hwc).to(cuda), torch.from_numpy(a).to(cuda),
+                                                **fgm.BASELINE_PARAMS.kwargs())
+    assert f_dev.is_cuda and f_dev.shape == (61, 97, 3) and str(f_dev.dtype) == f"torch.{dtype}"
+    # same fp32 solve; the host path rounds its fp64 input to fp32 the same way
+    assert np.array_equal(f_dev.double().cpu().numpy(), f_host)
+    assert np.array_equal(b_dev.double().cpu().numpy(), b_host)
+    with pytest.raises(ValueError, match="alpha size"):
+        fgm.ml_foreground_background(torch.from_numpy(hwc).to(cuda), torch.from_numpy(a[:9]).to(cuda))
+
+
+# ---- compose epilogue: image.cpp:39-57 -----------------
+def test_compose_vs_reference(fgm, cuda, ref, orc):
+    rng = np.random.default_rng(39)
+    f = rng.random((3, 37, 53), dtype=np.float32)
+    b = rng.random((3, 37, 53), dtype=np.float32)
+    a = (rng.random((37, 53), dtype=np.float32) * 1.4 - 0.2).astype(np.float32)  # clamping exercised
+    out = fgm.compose_cuda(dev(f, cuda), dev(b, cuda), dev(a, cuda)).cpu().numpy()
+    assert np.array_equal(out, orc.compose(f, b, a))  # same fp32 operation order, bitwise
+    assert np.abs(out - ref.compose(f, b, a)).max() < 1e-6  # the reference in fp64
+    with pytest.raises(ValueError, match="compose: alpha size"):
+        fgm.compose_cuda(dev(f, cuda), dev(b, cuda), dev(a[:5], cuda))
+
+
+def test_compose_estimate_reconstructs_image(fgm, cuda, orc):
+    # test_multilevel.cpp:239-261 through the device epilogue: compose(F, B, alpha) ~ I
+    from paper_2006_14970_b200 import synth
+    img, alpha = synth.make_composite(160, 96, synth.BASE_SEED + 5, ellipses=3, edge=4.0)
+    f, b = fgm.ml_foreground_background_cuda(img.to(cuda), alpha.to(cuda), fgm.BASELINE_PARAMS)
+    rec = fgm.compose_cuda(f, b, alpha.to(cuda))
+    assert float((rec - img.to(cuda)).abs().mean()) < 1e-3
+
+
 def test_resize_identity_and_errors(fgm, cuda):
     x = torch.rand(3, 6, 9, device=cuda)
     assert torch.equal(fgm.resize_cuda(x, 9, 6), x)

@@ -222,3 +222,10 @@ def test_fp32_restatement_drift_bounded(orc):
     f64, b64 = orc.ml_solve(img.astype(np.float64), a.astype(np.float64))
     f32, b32 = orc.ml_solve(img, a, dtype=np.float32)
     assert np.abs(f32 - f64).max() < 1e-3 and np.abs(b32 - b64).max() < 1e-3
+
+
+def test_compose_matches_reference(orc, ref):  # image.cpp:39-57
+    rng = np.random.default_rng(57)
+    f, b = rng.random((3, 11, 13)), rng.random((3, 11, 13))
+    a = rng.random((11, 13)) * 1.4 - 0.2
+    assert np.array_equal(orc.compose(f, b, a), ref.compose(f, b, a))
