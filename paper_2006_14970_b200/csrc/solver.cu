@@ -347,18 +347,33 @@ struct JobStage {
 // bands running at any moment belong to many images (no pipeline fill per
 // image) and every band's predecessor has a smaller ticket.
 // full: one item per band (full-channel kernel); else one per (band, channel).
+// Ticket order of a launch's bands: critical path first.  Band q of image i
+// can start ~q*lag steps after the image's band 0 (the boundary-stream lag of
+// 32 rows + a 16-column chunk) and the image's chain ends (nb-1)*lag + w steps
+// after that, so images get a start offset S_i = -((nb_i-1)*lag + w_i) and
+// tickets follow S_i + q*lag.  Within an image the order is q ascending (an
+// awaited band always holds an earlier ticket: no deadlock); the tall/wide
+// images' long chains start first instead of forming the launch's tail.
 std::vector<int2> band_order(const std::vector<SweepJob>& sj, bool full) {
-    int maxnb = 0;
-    for (const auto& j : sj) maxnb = std::max(maxnb, j.nb);
+    constexpr double lag = kBandRows + kChunk;
+    struct Key {
+        double k;
+        int i, q;
+    };
+    std::vector<Key> keys;
+    for (size_t i = 0; i < sj.size(); ++i) {
+        const double S = -((sj[i].nb - 1) * lag + sj[i].w);
+        for (int q = 0; q < sj[i].nb; ++q) keys.push_back({S + q * lag, int(i), q});
+    }
+    std::stable_sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) { return a.k < b.k; });
     std::vector<int2> ord;
-    for (int q = 0; q < maxnb; ++q)
-        for (size_t i = 0; i < sj.size(); ++i)
-            if (q < sj[i].nb) {
-                if (full)
-                    ord.push_back(make_int2(int(i), q));
-                else
-                    for (int c = 0; c < 3; ++c) ord.push_back(make_int2(int(i), 3 * q + c));
-            }
+    ord.reserve(keys.size() * (full ? 1 : 3));
+    for (const Key& k : keys) {
+        if (full)
+            ord.push_back(make_int2(k.i, k.q));
+        else
+            for (int c = 0; c < 3; ++c) ord.push_back(make_int2(k.i, 3 * k.q + c));
+    }
     return ord;
 }
 

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fgm_device.cuh"
 #include "fgm_internal.h"
@@ -584,6 +585,7 @@ cudaError_t launch_f(const SweepJob* jobs_dev, const int2* order_dev, int total_
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweepf_kernel<K, true>, 32, smem);
+        if (const char* e = std::getenv("FGM_FULL_WARPS_PER_SM")) per_sm = std::min(per_sm, std::atoi(e));  // tuning
         grid_cap = std::max(1, sms * std::max(1, per_sm));
     }
     const int grid = std::max(1, std::min(total_items, grid_cap));
