@@ -20,6 +20,8 @@
  *   fgm_resize_f32           <- fgmatte::resize              src/image.cpp:114-133
  *   fgm_ml_solve_hwc         <- _fgmatte.ml_foreground_background with its
  *                               HWC conversion loops     python/bindings.cpp:20-53,146-157
+ *   fgm_metrics_f32          <- fgmatte::evaluate_metrics    src/metrics.cpp:75-145
+ *
  *   fgm_compose_f32          <- fgmatte::compose             src/image.cpp:39-57
  *                               (python/bindings.cpp:89-95)
  *   fgm_sweep_passes_f32     <- `iterations` x sweep         src/multilevel.cpp:81-121, 162-163
@@ -107,6 +109,15 @@ int fgm_resize_f32(const float* src, int sw, int sh, int nplanes, float* dst, in
  * `stream` (zero-copy for torch / DLPack callers). */
 int fgm_ml_solve_hwc(const void* image_hwc, const void* alpha, int w, int h, int f64, const fgm_params* p,
                      void* fg_hwc, void* bg_hwc, void* stream);
+
+/* Quality metrics of an estimate against ground truth over the translucent
+ * region 0 < alpha < 1 (metrics.cpp:75-145): out[0] = SAD, out[1] = MSE (the
+ * reference's alpha-weighted sum), out[2] = GRAD (Gaussian-derivative filter,
+ * sigma, radius = kernel_radius or ceil(4 sigma)), out[3] = translucent pixel
+ * count.  fp64 accumulation, deterministic.  Device pointers in, host `out`;
+ * synchronises `stream`.  Errors as GradParams::validate (metrics.cpp:13-16). */
+int fgm_metrics_f32(const float* est, const float* gt, const float* alpha, int w, int h, int nch, double sigma,
+                    int kernel_radius, double* out, void* stream);
 
 /* Composite: out_c = clamp01(alpha * fg_c + (1 - alpha) * bg_c) for `nch`
  * planes (image.cpp:39-57); the epilogue that puts an estimated foreground on

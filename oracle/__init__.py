@@ -205,6 +205,7 @@ class _Reference:
                                           _ip, _ip, _ip, C.c_int]
         L.fgmr_resize.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, C.c_int, C.c_int]
         L.fgmr_compose.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, C.c_int, _dp]
+        L.fgmr_metrics.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _dp]
         L.fgmr_solve_pixel.argtypes = [C.c_double, _dp, C.c_int, _dp, _dp, _dp, C.c_double, C.c_double, C.c_int,
                                        _dp, _dp]
         L.fgmr_ml_solve.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
@@ -234,6 +235,15 @@ class _Reference:
         out = np.empty((nch, dh, dw))
         self._check(self.lib.fgmr_resize(_ptr(s, _dp), sw, sh, nch, _ptr(out, _dp), dw, dh))
         return out[0] if two_d else out
+
+    def metrics(self, est, gt, alpha, sigma=1.4, kernel_radius=0):
+        """evaluate_metrics (metrics.cpp:75-145): dict of sad, mse, grad, translucent_pixel_count."""
+        nch, h, w = est.shape
+        e, g, a = _f64(est), _f64(gt), _f64(alpha)
+        out = np.empty(4)
+        self._check(self.lib.fgmr_metrics(_ptr(e, _dp), _ptr(g, _dp), _ptr(a, _dp), w, h, nch, sigma, kernel_radius,
+                                          _ptr(out, _dp)))
+        return {"sad": out[0], "mse": out[1], "grad": out[2], "translucent_pixel_count": int(out[3])}
 
     def compose(self, fg, bg, alpha):
         nch, h, w = fg.shape

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "fgmatte/image.hpp"
+#include "fgmatte/metrics.hpp"
 #include "fgmatte/multilevel.hpp"
 
 using namespace fgmatte;
@@ -98,6 +99,27 @@ int fgmr_compose(const double* fg, const double* bg, const double* alpha, int w,
         std::memcpy(a.data().data(), alpha, sizeof(double) * n);
         const Image o = compose(f, b, a);
         std::memcpy(out, o.data().data(), sizeof(double) * n * size_t(nch));
+    });
+}
+
+// fgmatte::evaluate_metrics, metrics.cpp:75-145 (SAD, MSE, GRAD, translucent count)
+int fgmr_metrics(const double* est, const double* gt, const double* alpha, int w, int h, int nch, double sigma,
+                 int kernel_radius, double* out4) {
+    return run_guarded([&] {
+        const size_t n = size_t(w) * h;
+        Image e(w, h, nch), g(w, h, nch);
+        AlphaMatte a(w, h);
+        std::memcpy(e.data().data(), est, sizeof(double) * n * size_t(nch));
+        std::memcpy(g.data().data(), gt, sizeof(double) * n * size_t(nch));
+        std::memcpy(a.data().data(), alpha, sizeof(double) * n);
+        GradParams gp;
+        gp.sigma = sigma;
+        gp.kernel_radius = kernel_radius;
+        const MetricReport r = evaluate_metrics(e, g, a, gp);
+        out4[0] = r.sad;
+        out4[1] = r.mse;
+        out4[2] = r.grad;
+        out4[3] = double(r.translucent_pixel_count);
     });
 }
 

@@ -110,6 +110,8 @@ def _load():
                                            C.POINTER(vp)]
     L.fgm_resize_f32.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp]
     L.fgm_compose_f32.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp]
+    L.fgm_metrics_f32.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                  C.POINTER(C.c_double), vp]
     L.fgm_ml_solve_hwc.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, P, vp, vp, vp]
     L.fgm_sweep_passes_f32.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp, vp,
                                        vp]
@@ -400,6 +402,21 @@ def resize_cuda(src, width: int, height: int):
     _check(_load().fgm_resize_f32(src.data_ptr(), src.shape[2], src.shape[1], src.shape[0], out.data_ptr(), width,
                                   height, _stream_ptr(src.device)))
     return out
+
+
+def evaluate_metrics_cuda(est, gt, alpha, sigma: float = 1.4, kernel_radius: int = 0) -> dict:
+    """SAD / MSE / GRAD of an estimate against ground truth over the translucent
+    region (metrics.cpp:75-145, fgmatte::evaluate_metrics): (C, H, W) float32
+    CUDA tensors est, gt and (H, W) alpha_gt.  fp64 accumulation."""
+    est, gt, alpha = _dev_f32(est, "est"), _dev_f32(gt, "gt"), _dev_f32(alpha, "alpha")
+    if est.shape != gt.shape:
+        raise ValueError(f"sad: est {tuple(est.shape)} does not match gt {tuple(gt.shape)}")
+    if tuple(alpha.shape) != tuple(est.shape[1:]):
+        raise ValueError(f"sad: alpha size {tuple(alpha.shape)} does not match images {tuple(est.shape[1:])}")
+    out = (C.c_double * 4)()
+    _check(_load().fgm_metrics_f32(est.data_ptr(), gt.data_ptr(), alpha.data_ptr(), est.shape[2], est.shape[1],
+                                   est.shape[0], float(sigma), int(kernel_radius), out, _stream_ptr(est.device)))
+    return {"sad": out[0], "mse": out[1], "grad": out[2], "translucent_pixel_count": int(out[3])}
 
 
 def compose_cuda(fg, bg, alpha, out=None):

@@ -38,7 +38,10 @@ struct CoarseJob {
 
 // ---- K3: big-level sweep, skewed-band wavefront ---------------------------
 constexpr int kBandRows = 32;   // one warp = 32 skewed rows
-constexpr int kChunk = 16;      // boundary-stream polling granularity (columns)
+#ifndef FGM_CHUNK
+#define FGM_CHUNK 16
+#endif
+constexpr int kChunk = FGM_CHUNK;  // boundary-stream polling granularity (columns)
 constexpr unsigned kStreamSentinel = 0xFFFFFFFFu;  // a NaN: never a clamped output
 
 struct SweepJob {
@@ -92,6 +95,9 @@ cudaError_t launch_upsample(const ResampleJob* jobs_dev, int njobs, long long to
 bool upsample_ok(int sw, int sh, int dw, int dh);
 cudaError_t launch_hwc_to_planar(const void* src, bool f64, long long n, int ch, float* dst, cudaStream_t s);
 cudaError_t launch_planar_to_hwc(const float* src, long long n, int ch, void* dst, bool f64, cudaStream_t s);
+int metrics_blocks(long long n);
+cudaError_t launch_metrics(const float* est, const float* gt, const float* alpha, int w, int h, int nch,
+                           const double* kern, int r, double* partial, int blocks, cudaStream_t s);
 cudaError_t launch_compose(const float* fg, const float* bg, const float* alpha, long long n, int nch, float* out,
                            cudaStream_t s);  // scale within the staged window
 cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float omega, cudaStream_t s);

@@ -336,6 +336,82 @@ cudaError_t launch_planar_to_hwc(const float* src, long long n, int ch, void* ds
 }
 
 // ----------------------------------------------------------------------------
+// Quality metrics (metrics.cpp:75-145): alpha-weighted SAD, "MSE" (a weighted
+// sum) and the Gaussian-derivative gradient error over the translucent region
+// 0 < alpha < 1, in fp64 with the reference's per-pixel operation order (no
+// FMA contraction: __dmul_rn/__dadd_rn), one partial sum per block (summed on
+// the host in block order: deterministic).
+constexpr int kMetThreads = 256;
+
+__device__ __forceinline__ double conv_at(const float* p, int x, int y, int w, int h, bool along_x,
+                                          const double* kern, int r) {
+    double acc = 0.0;  // convolve_axis, metrics.cpp:35-57
+    for (int k = -r; k <= r; ++k) {
+        int xx = x, yy = y;
+        if (along_x) {
+            xx = x + k;
+            xx = xx < 0 ? 0 : (xx > w - 1 ? w - 1 : xx);
+        } else {
+            yy = y + k;
+            yy = yy < 0 ? 0 : (yy > h - 1 ? h - 1 : yy);
+        }
+        acc = __dadd_rn(acc, __dmul_rn(kern[k + r], double(p[(long long)yy * w + xx])));
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(kMetThreads) metrics_kernel(const float* __restrict__ est,
+                                                              const float* __restrict__ gt,
+                                                              const float* __restrict__ alpha, int w, int h, int nch,
+                                                              const double* __restrict__ kern, int r,
+                                                              double* __restrict__ partial) {
+    const long long n = (long long)w * h;
+    double s_sad = 0.0, s_mse = 0.0, s_grad = 0.0, s_cnt = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double a = double(alpha[i]);
+        if (!(a > 0.0 && a < 1.0)) continue;
+        const int x = int(i % w), y = int(i / w);
+        double d_abs = 0.0, d_sq = 0.0;
+        for (int c = 0; c < nch; ++c) {
+            const double e = __dadd_rn(double(est[c * n + i]), -double(gt[c * n + i]));
+            d_abs = __dadd_rn(d_abs, fabs(e));
+            d_sq = __dadd_rn(d_sq, __dmul_rn(e, e));
+        }
+        s_sad = __dadd_rn(s_sad, __dmul_rn(a, d_abs));
+        s_mse = __dadd_rn(s_mse, __dmul_rn(a, d_sq));
+        for (int c = 0; c < nch; ++c) {
+            const float* pe = est + c * n;
+            const float* pg = gt + c * n;
+            const double gx = __dadd_rn(conv_at(pe, x, y, w, h, true, kern, r), -conv_at(pg, x, y, w, h, true, kern, r));
+            const double gy =
+                __dadd_rn(conv_at(pe, x, y, w, h, false, kern, r), -conv_at(pg, x, y, w, h, false, kern, r));
+            s_grad = __dadd_rn(s_grad, __dmul_rn(a, __dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy))));
+        }
+        s_cnt += 1.0;
+    }
+    __shared__ double red[4][kMetThreads];
+    red[0][threadIdx.x] = s_sad;
+    red[1][threadIdx.x] = s_mse;
+    red[2][threadIdx.x] = s_grad;
+    red[3][threadIdx.x] = s_cnt;
+    __syncthreads();
+    for (int o = kMetThreads / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x < 4) partial[blockIdx.x * 4 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+int metrics_blocks(long long n) { return int(std::max<long long>(1, std::min<long long>((n + kMetThreads - 1) / kMetThreads, 148 * 8))); }
+
+cudaError_t launch_metrics(const float* est, const float* gt, const float* alpha, int w, int h, int nch,
+                           const double* kern, int r, double* partial, int blocks, cudaStream_t s) {
+    metrics_kernel<<<blocks, kMetThreads, 0, s>>>(est, gt, alpha, w, h, nch, kern, r, partial);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------
 // Compose epilogue (image.cpp:39-57): out = clamp01(a * f + (1 - a) * b) per
 // plane, in the reference's operation order (a*f, (1-a)*b, add; no FMA).
 __global__ void compose_kernel(const float* __restrict__ fg, const float* __restrict__ bg,

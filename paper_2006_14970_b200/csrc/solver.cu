@@ -1021,6 +1021,45 @@ int fgm_ml_solve_hwc(const void* image_hwc, const void* alpha, int w, int h, int
     });
 }
 
+int fgm_metrics_f32(const float* est, const float* gt, const float* alpha, int w, int h, int nch, double sigma,
+                    int kernel_radius, double* out, void* stream) {
+    return guarded([&] {
+        check_dims(w, h);
+        if (nch < 1) throw InvalidArgument("metrics: channels must be >= 1, got " + std::to_string(nch));
+        if (!est || !gt || !alpha || !out) throw InvalidArgument("metrics: null buffer");
+        // GradParams::validate (metrics.cpp:13-16), same messages
+        if (!(sigma > 0.0)) throw InvalidArgument("GradParams: sigma must be > 0");
+        const int r = kernel_radius > 0 ? kernel_radius : int(std::ceil(4.0 * sigma));
+        if (r < 1) throw InvalidArgument("GradParams: kernel radius must be >= 1");
+        require_device();
+        // gaussian_derivative_kernel (metrics.cpp:61-73), host fp64
+        std::vector<double> kern(size_t(2 * r + 1));
+        double ramp = 0.0;
+        for (int k = -r; k <= r; ++k) {
+            const double g = std::exp(-(double(k) * k) / (2.0 * sigma * sigma));
+            kern[size_t(k + r)] = double(k) * g;
+            ramp += double(k) * k * g;
+        }
+        for (double& x : kern) x /= ramp;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const int blocks = metrics_blocks((long long)w * h);
+        Arena A;
+        A.reserve(al(kern.size() * sizeof(double)) + al(size_t(blocks) * 4 * sizeof(double)), s);
+        double* dk = A.take<double>(kern.size());
+        double* dp = A.take<double>(size_t(blocks) * 4);
+        ck(cudaMemcpyAsync(dk, kern.data(), kern.size() * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+        ck(launch_metrics(est, gt, alpha, w, h, nch, dk, r, dp, blocks, s), "metrics_kernel");
+        std::vector<double> part(size_t(blocks) * 4);
+        ck(cudaMemcpyAsync(part.data(), dp, part.size() * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        for (int q = 0; q < 4; ++q) {
+            double acc = 0.0;
+            for (int b = 0; b < blocks; ++b) acc += part[size_t(b) * 4 + q];
+            out[q] = acc;
+        }
+    });
+}
+
 int fgm_compose_f32(const float* fg, const float* bg, const float* alpha, int w, int h, int nch, float* out,
                     void* stream) {
     return guarded([&] {

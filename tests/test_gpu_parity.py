@@ -189,6 +189,24 @@ def test_ml_foreground_background_device_hwc(fgm, cuda, dtype):
         fgm.ml_foreground_background(torch.from_numpy(hwc).to(cuda), torch.from_numpy(a[:9]).to(cuda))
 
 
+# ---- quality metrics: metrics.cpp:75-145 --------------
+def test_metrics_vs_reference(fgm, cuda, ref):
+    from paper_2006_14970_b200 import synth
+    img, alpha = synth.make_composite(131, 77, synth.BASE_SEED + 21, ellipses=4, edge=5.0)
+    f, b = fgm.ml_foreground_background_cuda(img.to(cuda), alpha.to(cuda), fgm.BASELINE_PARAMS)
+    rng = np.random.default_rng(4)
+    gt = torch.from_numpy(rng.random((3, 77, 131), dtype=np.float32)).to(cuda)
+    for sigma, radius in [(1.4, 0), (0.8, 3), (2.0, 0)]:
+        got = fgm.evaluate_metrics_cuda(f, gt, alpha.to(cuda), sigma, radius)
+        want = ref.metrics(f.double().cpu().numpy(), gt.double().cpu().numpy(), alpha.double().numpy(), sigma,
+                           radius)
+        assert got["translucent_pixel_count"] == want["translucent_pixel_count"] > 0
+        for k in ("sad", "mse", "grad"):
+            assert abs(got[k] - want[k]) <= 1e-12 * max(1.0, abs(want[k])), (k, got[k], want[k])
+    with pytest.raises(ValueError, match="GradParams: sigma must be > 0"):
+        fgm.evaluate_metrics_cuda(f, gt, alpha.to(cuda), 0.0)
+
+
 # ---- compose epilogue: image.cpp:39-57 -----------------
 def test_compose_vs_reference(fgm, cuda, ref, orc):
     rng = np.random.default_rng(39)
