@@ -44,6 +44,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fgm_device.cuh"
 #include "fgm_internal.h"
@@ -615,6 +616,7 @@ cudaError_t launch_sweep_k(const SweepJob* jobs_dev, const int2* order_dev, int 
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<K, true, kChunk>, 32, smem);
+        if (const char* e = std::getenv("FGM_SWEEP_WARPS_PER_SM")) per_sm = std::min(per_sm, std::atoi(e));  // tuning
         grid_cap = std::max(1, sms * std::max(1, per_sm));
     }
     if (total_items <= grid_cap)
