@@ -133,9 +133,12 @@ __global__ void __launch_bounds__(kResCols) resample_kernel(const ResampleJob* _
 // next tile's loads overlap this tile's interpolation; every output takes its
 // four taps from shared memory with compile-time plane offsets.  Same
 // arithmetic as resample_tile (bitwise identical results).
-constexpr int kUpCols = 128, kUpRows = 8, kUpThreads = 128;
+#ifndef FGM_UP_ROWS
+#define FGM_UP_ROWS 8
+#endif
+constexpr int kUpCols = 128, kUpRows = FGM_UP_ROWS, kUpThreads = 128;
 constexpr double kUpMaxScale = 0.625;
-constexpr int kUpSR = 8;   // ceil(7 * 0.625) + 3
+constexpr int kUpSR = (kUpRows - 1) * 5 / 8 + 4;  // >= ceil((rows-1) * 0.625) + 3
 constexpr int kUpSC = 83;  // ceil(127 * 0.625) + 3
 constexpr int kUpPlane = kUpSR * kUpSC;
 constexpr int kUpBuf = 6 * kUpPlane;
@@ -211,8 +214,8 @@ __global__ void __launch_bounds__(kUpThreads) upsample_kernel(const ResampleJob*
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;" ::: "memory");
         __syncthreads();  // this tile's window and taps are visible
         {
-            // thread = (lane l, row pair rp): columns x0 + l + 32i (i < 4), rows
-            // 2rp, 2rp+1.  Lanes read neighbouring (or equal) staged words:
+            // thread = (lane l, warp rp): columns x0 + l + 32i (i < 4), rows
+            // rp, rp + 4, ...  Lanes read neighbouring (or equal) staged words:
             // no bank conflicts; stores are 128-byte warp rows.
             const ResampleJob& J = jobs[cur.job];
             const int l = tid & 31, rp = tid >> 5;
@@ -228,8 +231,8 @@ __global__ void __launch_bounds__(kUpThreads) upsample_kernel(const ResampleJob*
             const float* buf = sm + b * kUpBuf;
             const long long dps = J.dpstride;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int rr = 2 * rp + h;
+            for (int h = 0; h < kUpRows / 4; ++h) {
+                const int rr = rp + 4 * h;
                 if (rr >= cur.nrows) break;
                 const Tap ty = tys[b][rr];
                 const float* ra = buf + (ty.i0 - cur.r0) * kUpSC;
