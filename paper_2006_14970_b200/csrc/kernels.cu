@@ -245,7 +245,8 @@ __global__ void __launch_bounds__(kUpThreads) upsample_kernel(const ResampleJob*
                     for (int p = 0; p < 6; ++p) {
                         const float* a = ra + p * kUpPlane + sa[i];
                         const float* c = rc + p * kUpPlane + sa[i];
-                        d[p * dps + 32 * i] = bilerp(a[0], a[dx[i]], c[0], c[dx[i]], tx[i], ty.t);
+                        // streaming store: the next level's sweep reads it once, much later
+                        __stcs(d + p * dps + 32 * i, bilerp(a[0], a[dx[i]], c[0], c[dx[i]], tx[i], ty.t));
                     }
                 }
             }
