@@ -120,19 +120,24 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def config_block(sizes, shard_mp):
+def config_block(sizes, shard_mp, world=1, scaling="weak"):
     from paper_2006_14970_b200 import synth
 
+    batch_mp = sum(w * h for w, h in sizes) / 1e6
+    weak = scaling == "weak"
     return {
         "workload": "C4: batch of 256 synthetic composites, sizes U{768x512,1024x1024,2048x1536,3000x2000} "
                     "(BASELINE.json configs[3]); multi-level solve per image",
-        "images": len(sizes),
-        "megapixels": round(sum(w * h for w, h in sizes) / 1e6, 3),
+        "images": len(sizes) * (world if weak else 1),
+        "images_per_rank": len(sizes) if weak else None,
+        "megapixels": round(batch_mp * (world if weak else 1), 3),
         "megapixels_this_rank": round(shard_mp, 3),
         "params": PARAMS,
         "seed": synth.BASE_SEED,
         "l2": "inputs larger than L2 (>10 GB of image+alpha per step vs 126 MB L2); no flush needed",
-        "sharding": "LPT by pixel count across ranks, no data-path collective",
+        "sharding": ("weak: every rank solves its own 256-image C4 batch (same sizes, image seeds offset by "
+                     "rank*256), no data-path collective" if weak else
+                     "strong: one 256-image batch split across ranks by LPT on pixel count, no data-path collective"),
     }
 
 
@@ -172,9 +177,9 @@ def run_reference(args, rank, world):
     ms = statistics.median([s for _, s in times]) * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(sizes, sum(w * h for w, h in sizes) / 1e6),
+        "config": config_block(sizes, sum(w * h for w, h in sizes) / 1e6, 1, args.scaling),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "reference", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -195,16 +200,24 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     params = fgm.Params(**PARAMS)
     sizes = synth.c4_sizes()
-    mine = shard.lpt_partition(sizes, world)[rank]
+    if args.scaling == "weak":
+        # the path partitions into independent images: every rank solves its
+        # own C4 batch (per-GPU work fixed as N grows)
+        mine = list(range(len(sizes)))
+        seed_of = lambda i: synth.BASE_SEED + 1000 + rank * len(sizes) + i  # noqa: E731
+        total_mp = world * sum(w * h for w, h in sizes) / 1e6
+    else:
+        mine = shard.lpt_partition(sizes, world)[rank]
+        seed_of = lambda i: synth.BASE_SEED + 1000 + i  # noqa: E731
+        total_mp = sum(w * h for w, h in sizes) / 1e6
     my_sizes = [sizes[i] for i in mine]
     my_mp = shard.shard_pixels(sizes, mine) / 1e6
-    total_mp = sum(w * h for w, h in sizes) / 1e6
 
     # inputs resident in HBM (generated on the device from the per-image seeds)
     imgs, alps = [], []
     for i in mine:
         w, h = sizes[i]
-        im, al = synth.make_composite(w, h, synth.BASE_SEED + 1000 + i, 5, 4.0, False, device=str(dev))
+        im, al = synth.make_composite(w, h, seed_of(i), 5, 4.0, False, device=str(dev))
         imgs.append(im)
         alps.append(al)
     outs = [(torch.empty_like(x), torch.empty_like(x)) for x in imgs]
@@ -279,9 +292,9 @@ def run_ours(args, rank, world, local):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": config_block(sizes, my_mp),
+            "config": config_block(sizes, my_mp, world, args.scaling),
             "e2e": {"value": total_mp / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "entry": "fgm_batch_solve_host_f32 (C ABI, pinned host buffers)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -306,6 +319,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: a 256-image C4 batch per GPU (default); strong: one batch split by LPT")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

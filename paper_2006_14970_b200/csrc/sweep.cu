@@ -446,6 +446,8 @@ __device__ __forceinline__ void acquire_chunk(float4 v, const float* up_stream, 
     using G = Geom<K, CK>;
     const int nvalid = min(CK, Umax - u0) * K * 2;  // floats
     const bool mine = lane < G::CH4 && 4 * lane < nvalid;
+    // (exponential back-off up to 4 us was measured: no effect on batches,
+    // slower single images)
     while (!__all_sync(kFull, chunk_complete<K, CK>(v, u0, Umax, lane))) {
         __nanosleep(32);
         if (mine) v = ld_relaxed_v4(up_stream + size_t(u0) * K * 2 + 4 * lane);
@@ -619,7 +621,12 @@ cudaError_t launch_sweep_k(const SweepJob* jobs_dev, const int2* order_dev, int 
         if (const char* e = std::getenv("FGM_SWEEP_WARPS_PER_SM")) per_sm = std::min(per_sm, std::atoi(e));  // tuning
         grid_cap = std::max(1, sms * std::max(1, per_sm));
     }
-    if (total_items <= grid_cap)
+    static int waves = -1;
+    if (waves < 0) {
+        const char* e = std::getenv("FGM_CHUNK4_WAVES");  // tuning knob
+        waves = e ? std::atoi(e) : 1;
+    }
+    if (total_items <= waves * grid_cap)
         return launch_sweep_kc<K, 4>(jobs_dev, order_dev, total_items, ticket, eps, omega, s, grid_cap);
     return launch_sweep_kc<K, kChunk>(jobs_dev, order_dev, total_items, ticket, eps, omega, s, grid_cap);
 }
