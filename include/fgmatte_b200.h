@@ -132,9 +132,10 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
                          int h, int iterations, double regularization, double gradient_weight, float* fg_out,
                          float* bg_out, void* stream);
 
-/* Big-level sweep kernel choice: 0 = automatic (per-channel warps while they
- * fit on the GPU, full-channel warps for larger launches), 1 = always
- * per-channel, 2 = always full-channel.  Both produce identical results. */
+/* Big-level sweep kernel choice (tuning; all produce bitwise identical results):
+ * 0 = automatic (per-(band, channel) warps), 1 = per-(band, channel) warps,
+ * 2 = full-channel warps (coefficients once per pixel, handed down by shuffle),
+ * 3 = band CTAs: three channel warps fed by one coefficient warp (K <= 2). */
 void fgm_set_sweep_mode(int mode);
 
 /* Profiling: when enabled, every kernel launch of the solver is bracketed by

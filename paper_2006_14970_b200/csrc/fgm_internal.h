@@ -110,6 +110,10 @@ cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, bool 
                                cudaStream_t s);
 // The full-channel (throughput) sweep kernel, same contract as launch_sweep;
 // order_dev holds (job, band) pairs.
+// band-CTA kernel (sweep_cta.cu): one ticket per band, per-channel streams
+int sweep_cta_supported_k(int K);
+cudaError_t launch_sweep_cta(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands,
+                             unsigned* ticket, float eps, float omega, cudaStream_t s);
 cudaError_t launch_sweep_full(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands,
                               unsigned* ticket, float eps, float omega, cudaStream_t s);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);

@@ -377,22 +377,33 @@ std::vector<int2> band_order(const std::vector<SweepJob>& sj, bool full) {
     return ord;
 }
 
-// Kernel choice per sweep launch.  Auto picks the per-(band, channel) kernel:
-// with pitched (16-byte) level rows the two measure within 3% on the C4 batch
-// (25.2 vs 25.9 ms of sweep), per-channel ahead.  The full-channel kernel
-// (bitwise identical) stays selectable with fgm_set_sweep_mode(2).
-int g_sweep_mode = 0;  // 0 auto, 1 always per-channel, 2 always full-channel
-bool use_full_kernel(int total_bands, int K) {
+// Kernel choice per sweep launch: 0 per-(band, channel) warps (sweep.cu),
+// 1 full-channel warps (sweep_full.cu), 2 band CTAs with a shared
+// coefficient warp (sweep_cta.cu).  All three are bitwise identical.
+int g_sweep_mode = 0;  // 0 auto, 1 per-channel, 2 full-channel, 3 band CTA
+int sweep_kind(int total_bands, int K) {
     (void)total_bands;
-    if (K > 3) return false;  // the full-channel kernel's state does not fit in registers beyond K = 3
-    return g_sweep_mode == 2;
+    if (g_sweep_mode == 2 && K <= 3) return 1;  // the full-channel kernel's state does not fit beyond K = 3
+    if (g_sweep_mode == 3 && sweep_cta_supported_k(K)) return 2;
+    return 0;
+}
+// one ticket per band (kinds 1, 2) or per (band, channel) (kind 0)
+inline bool per_band(int kind) { return kind != 0; }
+
+cudaError_t launch_sweep_kind(int kind, int K, const SweepJob* jd, const int2* od, int bands, unsigned* ticket,
+                              float eps, float omega, cudaStream_t s) {
+    switch (kind) {
+        case 1: return launch_sweep_full(K, jd, od, bands, ticket, eps, omega, s);
+        case 2: return launch_sweep_cta(K, jd, od, bands, ticket, eps, omega, s);
+        default: return launch_sweep(K, jd, od, 3 * bands, ticket, eps, omega, s);
+    }
 }
 
 enum LaunchKind { kCoarse, kResample, kUpsample, kSweep, kCopy };
 struct LaunchRec {
     LaunchKind kind;
     int K, njobs, total_bands;
-    bool full;
+    int skind;  // sweep kernel kind (sweep_kind)
     size_t job_off, ticket, order_off;
     long long max_rows;
     double bytes;
@@ -634,11 +645,10 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                     --st.counters;
                     continue;
                 }
-                const bool full = use_full_kernel(total, K);
+                const int sk = sweep_kind(total, K);
                 const size_t off = st.push(sj);
-                const size_t ooff = st.push(band_order(sj, full));
-                LaunchRec lr{kSweep, K, int(sj.size()), full ? total : 3 * total, full, off, ticket, ooff,
-                             (long long)max_stream, sbytes};
+                const size_t ooff = st.push(band_order(sj, per_band(sk)));
+                LaunchRec lr{kSweep, K, int(sj.size()), total, sk, off, ticket, ooff, (long long)max_stream, sbytes};
                 if (pi == 0 && has_ia[size_t(j)]) lr.ev = j;  // this step's I/alpha pyramid level
                 launches.push_back(lr);
             }
@@ -708,19 +718,17 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 break;
             }
             case kSweep: {
-                ck(launch_stream_fill(reinterpret_cast<const SweepJob*>(djobs + r.job_off), r.njobs, r.K, r.full,
+                ck(launch_stream_fill(reinterpret_cast<const SweepJob*>(djobs + r.job_off), r.njobs, r.K, r.skind == 1,
                                       size_t(r.max_rows), s),
                    "stream_fill_kernel");
                 if (std::getenv("FGM_DEBUG_SWEEP"))
-                    std::fprintf(stderr, "[fgm] sweep K=%d jobs=%d items=%d full=%d\n", r.K, r.njobs, r.total_bands,
-                                 int(r.full));
+                    std::fprintf(stderr, "[fgm] sweep K=%d jobs=%d bands=%d kind=%d\n", r.K, r.njobs, r.total_bands,
+                                 r.skind);
                 ProfScope ps(s, 0, r.bytes);
                 const SweepJob* jd = reinterpret_cast<const SweepJob*>(djobs + r.job_off);
                 const int2* od = reinterpret_cast<const int2*>(djobs + r.order_off);
-                if (r.full)
-                    ck(launch_sweep_full(r.K, jd, od, r.total_bands, dctr + r.ticket, eps, omega, s), "sweep_kernel");
-                else
-                    ck(launch_sweep(r.K, jd, od, r.total_bands, dctr + r.ticket, eps, omega, s), "sweep_kernel");
+                ck(launch_sweep_kind(r.skind, r.K, jd, od, r.total_bands, dctr + r.ticket, eps, omega, s),
+                   "sweep_kernel");
                 break;
             }
             case kCopy:  // njobs = width, total_bands = rows, max_rows = source pitch (floats)
@@ -1126,22 +1134,17 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
             ck(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s), "memset");
             SweepJob* d = A.take<SweepJob>(1);
             ck(cudaMemcpyAsync(d, &J1, sizeof(J1), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
-            const bool full = use_full_kernel(J1.nb, ps[pi]);
-            const std::vector<int2> ord = band_order({J1}, full);
+            const int sk = sweep_kind(J1.nb, ps[pi]);
+            const std::vector<int2> ord = band_order({J1}, per_band(sk));
             int2* dord = A.take<int2>(ord.size());
             ck(cudaMemcpyAsync(dord, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice, s),
                "cudaMemcpyAsync(order)");
-            ck(launch_stream_fill(d, 1, ps[pi], full, sf, s), "stream_fill_kernel");
+            ck(launch_stream_fill(d, 1, ps[pi], sk == 1, sf, s), "stream_fill_kernel");
             {
                 ProfScope pr(s, 0, 64.0 * double(px));
-                if (full)
-                    ck(launch_sweep_full(ps[pi], d, dord, J1.nb, ctr, float(regularization), float(gradient_weight),
-                                         s),
-                       "sweep_kernel");
-                else
-                    ck(launch_sweep(ps[pi], d, dord, 3 * J1.nb, ctr, float(regularization), float(gradient_weight),
-                                    s),
-                       "sweep_kernel");
+                ck(launch_sweep_kind(sk, ps[pi], d, dord, J1.nb, ctr, float(regularization), float(gradient_weight),
+                                     s),
+                   "sweep_kernel");
             }
             fi = J1.fg_out;
             bi = J1.bg_out;
@@ -1149,7 +1152,7 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
     });
 }
 
-void fgm_set_sweep_mode(int mode) { g_sweep_mode = (mode >= 0 && mode <= 2) ? mode : 0; }
+void fgm_set_sweep_mode(int mode) { g_sweep_mode = (mode >= 0 && mode <= 3) ? mode : 0; }
 
 void fgm_profile_enable(int on) {
     std::lock_guard<std::mutex> g(g_prof_mu);

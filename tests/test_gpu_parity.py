@@ -369,10 +369,13 @@ def test_sweep_kernels_agree_bitwise(fgm, cuda, oracle_mod, kw):
         a = fgm.batch_solve_cuda(imgs, alps, p)
         fgm.set_sweep_mode(2)
         b = fgm.batch_solve_cuda(imgs, alps, p)
+        fgm.set_sweep_mode(3)  # band CTAs with a shared coefficient warp
+        c = fgm.batch_solve_cuda(imgs, alps, p)
     finally:
         fgm.set_sweep_mode(0)
-    for (fa, ba), (fb, bb) in zip(a, b):
+    for (fa, ba), (fb, bb), (fc, bc) in zip(a, b, c):
         assert torch.equal(fa, fb) and torch.equal(ba, bb)
+        assert torch.equal(fa, fc) and torch.equal(ba, bc)
 
 
 def test_full_channel_kernel_vs_oracle(fgm, cuda, orc, oracle_mod):
