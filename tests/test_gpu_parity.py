@@ -391,3 +391,40 @@ def test_full_channel_kernel_vs_oracle(fgm, cuda, orc, oracle_mod):
             assert_close("bg", b, ob)
     finally:
         fgm.set_sweep_mode(0)
+
+
+# ---- reentrancy: concurrent solves from several host threads ----
+def test_concurrent_host_threads(fgm, cuda):
+    import threading
+    from paper_2006_14970_b200 import synth
+
+    cases = [synth.make_composite(w, h, 900 + i, 3, 3.0) for i, (w, h) in
+             enumerate([(300, 200), (257, 513), (640, 96), (128, 128), (1000, 40), (77, 333)])]
+    want = []
+    for img, a in cases:
+        f, b = fgm.ml_foreground_background_cuda(img.to(cuda), a.to(cuda), fgm.BASELINE_PARAMS)
+        want.append((f.cpu(), b.cpu()))
+    got = [None] * len(cases)
+    errs = []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream(cuda)
+            with torch.cuda.stream(s):
+                img, a = cases[i]
+                for _ in range(3):
+                    f, b = fgm.ml_foreground_background_cuda(img.to(cuda, non_blocking=False), a.to(cuda),
+                                                             fgm.BASELINE_PARAMS)
+                s.synchronize()
+                got[i] = (f.cpu(), b.cpu())
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(cases))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for (wf, wb), (gf, gb) in zip(want, got):
+        assert torch.equal(wf, gf) and torch.equal(wb, gb)
