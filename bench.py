@@ -267,11 +267,16 @@ def run_ours(args, rank, world, local):
     peak, peak_kind = peaks()
     sw = stats["sweep"]
     achieved = sw["alg_bytes"] / (sw["ms"] / 1e3) / 1e9 if sw["ms"] > 0 else 0.0
-    traffic = None
+    traffic, issue = None, None
     tpath = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("dram_bytes_per_launch")
+        if tj.get("sm_ipc"):  # the bound that actually binds K3
+            issue = {"bound": "issue", "achieved": tj["sm_ipc"], "peak": tj["sm_ipc_peak"],
+                     "unit": "warp-instructions/cycle/SM", "frac": tj["sm_ipc"] / tj["sm_ipc_peak"],
+                     "source": "ncu --set full of the top-level K3 launch (profiles/sweep_traffic.json)"}
     # profiled kernels (sweep, resample/upsample, coarse) plus one sentinel
     # fill per sweep launch
     launches = int((sum(v["launches"] for v in stats.values()) + stats["sweep"]["launches"]) // max(args.steps, 1))
@@ -302,7 +307,8 @@ def run_ours(args, rank, world, local):
                          "kernel": "sweep_kernel<2> (K3)", "peak_kind": peak_kind,
                          "alg_bytes_per_px_pass": 64,
                          "kernel_ms_per_step": sw["ms"] / args.steps,
-                         "kernel_launches_per_step": sw["launches"] / args.steps},
+                         "kernel_launches_per_step": sw["launches"] / args.steps,
+                         "issue": issue},
             "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in stats.items()},
             "cpu_baseline": cpu,
             "gpu_launches": launches,
