@@ -76,6 +76,8 @@ def full(rep, out, traffic=None, alg=None):
         info = {"kernel": d["Kernel Name"], "report": rep, "dram_bytes_per_launch": tb,
                 "alg_bytes_per_launch": float(alg) if alg else None,
                 "traffic_over_alg": tb / float(alg) if alg else None,
+                "sm_ipc": float(d["sm__inst_executed.avg.per_cycle_active"]), "sm_ipc_peak": 4.0,
+                "warp_instructions_per_launch": float(d["smsp__inst_executed.sum"]),
                 "note": "top-level K3 launch of the C4 batch (tools/prof_batch.py 256), ncu --set full"}
         json.dump(info, open(traffic, "w"), indent=1)
         print(info)
