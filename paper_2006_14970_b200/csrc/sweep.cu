@@ -254,7 +254,7 @@ __device__ __forceinline__ constexpr int ring(int off, int row, int dp) {
 // Coefficients of slot k's pixel of the next step (column offset 1 - k from
 // t - lane), its left edge weight `dL` given.  G: clamp neighbours at the
 // image border.
-template <int K, bool G>
+template <int K, bool G, bool Y = false, bool XL = false>
 __device__ __forceinline__ Coef1 next_coef(int rc, int k, float dL, int x, int y, int w, int h, float eps,
                                            float omega) {
     using Gm = Geom<K>;
@@ -265,9 +265,13 @@ __device__ __forceinline__ Coef1 next_coef(int rc, int k, float dL, int x, int y
     float aU = lds(rc + ring<K>(Gm::OFF_A, ar - 1, dp));
     float aD = lds(rc + ring<K>(Gm::OFF_A, ar + 1, dp));
     const float I = lds(rc + ring<K>(Gm::OFF_I, K - 1 - k, dp));
-    if (G) {
+    if (G || XL) {
         if (x <= 0) dL = eps;  // edge_weight(a, a)
+    }
+    if (G) {
         if (x >= w - 1) aR = a;
+    }
+    if (G || Y) {
         if (y <= 0) aU = a;
         if (y >= h - 1) aD = a;
     }
@@ -309,7 +313,14 @@ struct StepCtx {
 
 // One wavefront step.  G: a pixel of this step or the next may be on the
 // image border (clamped neighbours) or an output row segment may be partial.
-template <int K, bool G, int CK>
+// Y (with G false): interior columns of a band touching row 0 or h-1: only
+// the row clamps and the output row bounds of G (the first band heads every
+// image's chain, so it must not run at border-path speed).
+// XL (with G false): the first steps of a band, where only the left column
+// border occurs (x <= 0): the L clamp and the bounds of the stream and the
+// flush, as selects and predicates.  Every band's start is on the chain's
+// critical path (the band below waits for it).
+template <int K, bool G, int CK, bool Y = false, bool XL = false>
 __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_, int tr) {
     using Gm = Geom<K, CK>;
     constexpr int OW = Gm::OW;
@@ -341,15 +352,21 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
             R = recv[k - 1];
             D = st.outp[k - 1];
         }
-        if (G) {
+        if (G || Y || XL) {
             const int x = xs0 - k, y = y0 + lane - k;
             const float2 self = k == 0 ? make_float2(lds(rc + ring<K>(Gm::OFF_F, 0, Gm::SH)),
                                                      lds(rc + ring<K>(Gm::OFF_B, 0, Gm::SH)))
                                        : st.rprev[k > 0 ? k - 1 : 0];
-            if (!(x > 0)) L = self;
-            if (!(x < w - 1)) R = self;
-            if (!(y > 0)) U = self;
-            if (!(y < h - 1)) D = self;
+            if (G || XL) {
+                if (!(x > 0)) L = self;
+            }
+            if (G) {
+                if (!(x < w - 1)) R = self;
+            }
+            if (G || Y) {
+                if (!(y > 0)) U = self;
+                if (!(y < h - 1)) D = self;
+            }
         }
         nv[k] = pixel_apply1(st.co[k], L, R, U, D);
     }
@@ -357,7 +374,7 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
     // coefficients of the next step's pixels; dL = this step's dR of the slot
 #pragma unroll
     for (int k = 0; k < K; ++k)
-        st.co[k] = next_coef<K, G>(rc, k, st.co[k].dR, xs0 + 1 - k, y0 + lane - k, w, h, x_.eps, x_.omega);
+        st.co[k] = next_coef<K, G, Y, XL>(rc, k, st.co[k].dR, xs0 + 1 - k, y0 + lane - k, w, h, x_.eps, x_.omega);
 
     // output ring (last sweep only): column x & 15 == c & 15
     {
@@ -366,7 +383,7 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
             const int x = xs0 - (K - 1);
             ok = x >= 0 && x < w && y0 + lane - (K - 1) >= 0 && y0 + lane - (K - 1) < h;
         }
-        if (ok) {
+        if (ok) {  // (Y: rows outside the image land in the ring but are never flushed)
             const int o = x_.ob + (c & (OW - 1));
             sts(o, nv[K - 1].x);
             sts(o + Gm::OPL, nv[K - 1].y);
@@ -374,7 +391,7 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
     }
 
     // boundary stream for the band below: lane 31's K outputs of this step
-    if (x_.has_down && lane == kBandRows - 1 && (!G || (tr - 31 >= 0 && tr - 31 < x_.Umax))) {
+    if (x_.has_down && lane == kBandRows - 1 && (!(G || XL) || (tr - 31 >= 0 && tr - 31 < x_.Umax))) {
         float* dst = x_.my_stream + size_t(tr - 31) * K * 2;
         if (K % 2 == 0) {  // 16-byte aligned: u * 2K floats with K even
 #pragma unroll
@@ -399,6 +416,12 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
         if (G) {
             const int yf = y0 + jf - (K - 1);
             ok = xs >= 0 && xs + OW - 1 < w && yf >= 0 && yf < h;
+        } else {
+            if (Y) {
+                const int yf = y0 + jf - (K - 1);
+                ok = yf >= 0 && yf < h;
+            }
+            if (XL) ok = ok && xs >= 0;
         }
         if (ok) {  // off >= 0 here: unsigned, one IMAD.WIDE.U32 per plane
             const unsigned off = unsigned(jf * x_.opitch + xs + col);
@@ -421,7 +444,7 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
 
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        if (G) st.rprev[k] = recv[k];
+        if (G || Y || XL) st.rprev[k] = recv[k];
         st.outp[k] = nv[k];
     }
 }
@@ -448,16 +471,32 @@ __device__ __forceinline__ void acquire_chunk(float4 v, const float* up_stream, 
     const bool mine = lane < G::CH4 && 4 * lane < nvalid;
     // (exponential back-off up to 4 us was measured: no effect on batches,
     // slower single images)
+#ifndef FGM_POLL_NS
+#define FGM_POLL_NS 32
+#endif
     while (!__all_sync(kFull, chunk_complete<K, CK>(v, u0, Umax, lane))) {
-        __nanosleep(32);
+        if (FGM_POLL_NS) __nanosleep(FGM_POLL_NS);
         if (mine) v = ld_relaxed_v4(up_stream + size_t(u0) * K * 2 + 4 * lane);
     }
     if (mine) sts4(chunk + 4 * lane, v);
 }
 
+#ifdef FGM_TRACE
+__device__ unsigned long long g_trace[4 * 65536];  // per item: start, first chunk, fast phase, end (ns)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 template <int K, bool V4, int CK>
 __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int lane, unsigned sbase, float eps,
                                          float omega) {
+#ifdef FGM_TRACE
+    const int titem = (J.band_base + q) * 3 + ch;
+    if (lane == 0 && titem < 65536) g_trace[4 * titem] = gtimer();
+#endif
     using Gm = Geom<K, CK>;
     const int w = J.w, h = J.h;
     const int y0 = q * kBandRows;
@@ -529,6 +568,10 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
                 const int nxt = (t4 & ~(CK - 1)) + CK;  // the next chunk's first column
                 if ((t4 % CK) == 0) {
                     acquire_chunk<K, CK>(pend, up_stream, t4, Umax, lane, Gm::OFF_C);
+#ifdef FGM_TRACE
+                    if (t4 == 0 && lane == 0 && titem < 65536) g_trace[4 * titem + 1] = gtimer();
+                    if (t4 == 64 && lane == 0 && titem < 65536) g_trace[4 * titem + 2] = gtimer();
+#endif
                     pend_ok = false;
                     if (nxt < Umax && lane_ch)  // prefetch the next chunk
                         pend = ld_relaxed_v4(up_stream + size_t(nxt) * K * 2 + 4 * lane);
@@ -540,9 +583,20 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
                 }
             }
             __syncwarp();
-            if (!yband && t4 >= fast_lo && t4 + 4 <= fast_hi) {
+            if (t4 >= fast_lo && t4 + 4 <= fast_hi && !yband) {
 #pragma unroll
                 for (int s = 0; s < 4; ++s) band_step<K, false, CK>(st, cx, t4 + s);
+            } else if (t4 >= fast_lo && t4 + 4 <= fast_hi) {
+#pragma unroll
+                for (int s = 0; s < 4; ++s) band_step<K, false, CK, true>(st, cx, t4 + s);
+            } else if (t4 < fast_lo && t4 + 4 <= fast_hi) {  // band start: left border only
+                if (yband) {
+#pragma unroll
+                    for (int s = 0; s < 4; ++s) band_step<K, false, CK, true, true>(st, cx, t4 + s);
+                } else {
+#pragma unroll
+                    for (int s = 0; s < 4; ++s) band_step<K, false, CK, false, true>(st, cx, t4 + s);
+                }
             } else {
 #pragma unroll 1
                 for (int s = 0; s < 4; ++s) band_step<K, true, CK>(st, cx, t4 + s);
@@ -560,6 +614,9 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     }
     cp_wait<0>();
     __syncwarp();
+#ifdef FGM_TRACE
+    if (lane == 0 && titem < 65536) g_trace[4 * titem + 3] = gtimer();
+#endif
 }
 
 #ifndef FGM_SWEEP_MINB
@@ -626,8 +683,11 @@ cudaError_t launch_sweep_k(const SweepJob* jobs_dev, const int2* order_dev, int 
         const char* e = std::getenv("FGM_CHUNK4_WAVES");  // tuning knob
         waves = e ? std::atoi(e) : 1;
     }
+#ifndef FGM_LAT_CHUNK
+#define FGM_LAT_CHUNK 4
+#endif
     if (total_items <= waves * grid_cap)
-        return launch_sweep_kc<K, 4>(jobs_dev, order_dev, total_items, ticket, eps, omega, s, grid_cap);
+        return launch_sweep_kc<K, FGM_LAT_CHUNK>(jobs_dev, order_dev, total_items, ticket, eps, omega, s, grid_cap);
     return launch_sweep_kc<K, kChunk>(jobs_dev, order_dev, total_items, ticket, eps, omega, s, grid_cap);
 }
 
@@ -651,6 +711,12 @@ cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, bool 
 }
 
 int sweep_supported_k(int K) { return K >= 1 && K <= 4; }
+
+#ifdef FGM_TRACE
+extern "C" int fgm_debug_trace(unsigned long long* out, int n) {
+    return int(cudaMemcpyFromSymbol(out, g_trace, size_t(n) * sizeof(unsigned long long)));
+}
+#endif
 
 size_t sweep_smem_bytes(int K) {
     switch (K) {
