@@ -230,6 +230,12 @@ def run_ours(args, rank, world, local):
 
     for _ in range(args.warmup):
         fgm.batch_solve_cuda(imgs, alps, params, outputs=outs)
+    # fill the profiler's event pool with as many events as the timed steps use,
+    # so no event is created inside the timed region
+    with fgm.profile():
+        for _ in range(args.steps):
+            fgm.batch_solve_cuda(imgs, alps, params, outputs=outs)
+        torch.cuda.synchronize(dev)
     barrier()
 
     # ---- device-timed steps (K3 launches bracketed by events for the roofline)

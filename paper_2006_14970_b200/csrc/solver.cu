@@ -106,22 +106,34 @@ std::vector<ProfRec> g_prof;
 long long g_launches[3] = {0, 0, 0};
 double g_ms[3] = {0, 0, 0}, g_bytes[3] = {0, 0, 0};
 
+// Events come from a free list (created once, reused after each drain) so
+// that profiling adds no host-side event creation to the timed launches.
+std::vector<cudaEvent_t> g_ev_free;
+
+cudaEvent_t prof_event() {  // caller holds g_prof_mu
+    if (!g_ev_free.empty()) {
+        cudaEvent_t e = g_ev_free.back();
+        g_ev_free.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
 struct ProfScope {
     cudaEvent_t a = nullptr, b = nullptr;
     cudaStream_t s;
     int which;
     double bytes;
     ProfScope(cudaStream_t s_, int which_, double bytes_) : s(s_), which(which_), bytes(bytes_) {
-        bool on;
         {
             std::lock_guard<std::mutex> g(g_prof_mu);
-            on = g_prof_on;
+            if (!g_prof_on) return;
+            a = prof_event();
+            b = prof_event();
         }
-        if (on) {
-            ck(cudaEventCreate(&a), "cudaEventCreate");
-            ck(cudaEventCreate(&b), "cudaEventCreate");
-            ck(cudaEventRecord(a, s), "cudaEventRecord");
-        }
+        ck(cudaEventRecord(a, s), "cudaEventRecord");
     }
     ~ProfScope() {
         if (!a) return;
@@ -140,8 +152,8 @@ void prof_drain() {
         g_launches[r.which] += 1;
         g_ms[r.which] += ms;
         g_bytes[r.which] += r.bytes;
-        cudaEventDestroy(r.a);
-        cudaEventDestroy(r.b);
+        g_ev_free.push_back(r.a);
+        g_ev_free.push_back(r.b);
     }
     g_prof.clear();
 }
