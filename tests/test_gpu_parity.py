@@ -42,7 +42,8 @@ def test_golden_fixtures(fgm, cuda, oracle_mod, path):
 
 # ---- shapes, ragged edges and parameter variants vs the fp64 oracle --------
 SHAPES = [(1, 1), (2, 1), (1, 2), (3, 3), (5, 3), (1, 40), (40, 1), (31, 24), (45, 45), (46, 46), (64, 64), (65, 33),
-          (33, 65), (97, 53), (130, 9), (9, 130), (200, 136), (333, 517), (517, 333), (512, 512)]
+          (33, 65), (97, 53), (130, 9), (9, 130), (200, 136), (333, 517), (517, 333), (512, 512),
+          (7, 100), (37, 65), (39, 200), (12, 300)]
 
 
 @pytest.mark.parametrize("w,h", SHAPES)
@@ -72,6 +73,27 @@ def test_ml_vs_oracle_params(fgm, cuda, orc, oracle_mod, kw):
     of, ob = orc.ml_solve(img.astype(np.float64), a.astype(np.float64), p)
     assert_close("fg", f, of)
     assert_close("bg", b, ob)
+
+
+@pytest.mark.parametrize("w,h", [(7, 100), (37, 65), (39, 200), (40, 33), (41, 31), (64, 97), (300, 32), (300, 33)])
+def test_sweep_border_modes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h):
+    # narrow levels and bands at the row borders: the border / row-border /
+    # band-start variants of K3 (sweep.cu) against the fp64 oracle, level by
+    # level through the single-level entry (BASELINE params, K = 1..4)
+    rng = np.random.default_rng(w * 1000 + h)
+    img = rng.random((3, h, w)).astype(np.float32)
+    a = rng.random((h, w)).astype(np.float32)
+    f0 = rng.random((3, h, w)).astype(np.float32)
+    b0 = rng.random((3, h, w)).astype(np.float32)
+    p = oracle_mod.Params()
+    for K in (1, 2, 3, 4):
+        of, ob = orc.sweep(img.astype(np.float64), a.astype(np.float64), f0.astype(np.float64),
+                           b0.astype(np.float64), p, K)
+        gf, gb = fgm.sweep_passes_cuda(dev(img, cuda), dev(a, cuda), dev(f0, cuda), dev(b0, cuda), K, p.eps_r,
+                                       p.omega)
+        torch.cuda.synchronize()
+        assert_close("fg", gf.double().cpu().numpy(), of, tol_max=2e-5, tol_mean=1e-6)
+        assert_close("bg", gb.double().cpu().numpy(), ob, tol_max=2e-5, tol_mean=1e-6)
 
 
 def test_random_inputs_vs_oracle(fgm, cuda, orc, oracle_mod):
