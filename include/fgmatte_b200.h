@@ -141,12 +141,17 @@ void fgm_set_sweep_mode(int mode);
 /* Profiling: when enabled, every kernel launch of the solver is bracketed by
  * CUDA events on its stream; fgm_kernel_stats() synchronises on the recorded
  * events and reports, for kernel class `which` (0 = big-level sweep K3,
- * 1 = resample K1/K2, 2 = coarse levels K4), the launch count, the summed
- * device milliseconds and the algorithmic HBM bytes of those launches
+ * 1 = I/alpha pyramid K1, 2 = coarse levels K4, 3 = F/B upsample K2), the
+ * launch count, the summed device milliseconds and the algorithmic HBM bytes
+ * of those launches
  * ("Roofline").  fgm_profile_reset() clears the counters. */
 void fgm_profile_enable(int on);
 void fgm_profile_reset(void);
 int fgm_kernel_stats(int which, long long* launches, double* ms, double* alg_bytes);
+/* Diagnostic: the launches of the last drained profile window, in enqueue
+ * order: kernel class, start and end (ms from the first launch's start).
+ * Writes at most `max` entries; returns the number of launches. */
+int fgm_profile_timeline(int max, int* which, double* t0, double* t1);
 
 const char* fgm_last_error(void);
 int fgm_device_count(void);

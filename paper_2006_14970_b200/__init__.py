@@ -119,6 +119,7 @@ def _load():
     L.fgm_set_sweep_mode.argtypes = [C.c_int]
     L.fgm_kernel_stats.argtypes = [C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]
+    L.fgm_profile_timeline.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double)]
     _lib = L
     return L
 
@@ -455,7 +456,7 @@ class profile:
     """Context manager: per-kernel-class device time and algorithmic bytes of
     every launch inside the block (CUDA events on the launching stream)."""
 
-    NAMES = {0: "sweep", 1: "resample", 2: "coarse"}
+    NAMES = {0: "sweep", 1: "resample", 2: "coarse", 3: "upsample"}
 
     def __enter__(self):
         L = _load()
@@ -476,3 +477,13 @@ class profile:
             _check(L.fgm_kernel_stats(k, C.byref(n), C.byref(ms), C.byref(b)))
             out[name] = {"launches": n.value, "ms": ms.value, "alg_bytes": b.value}
         return out
+
+    @staticmethod
+    def timeline():
+        """[(class name, start ms, end ms)] of the last profiled window's
+        launches in enqueue order (times from the first launch's start)."""
+        L = _load()
+        n = L.fgm_profile_timeline(0, None, None, None)
+        w, a, b = (C.c_int * n)(), (C.c_double * n)(), (C.c_double * n)()
+        L.fgm_profile_timeline(n, w, a, b)
+        return [(profile.NAMES[w[i]], a[i], b[i]) for i in range(n)]

@@ -187,6 +187,98 @@ __device__ __forceinline__ float2 pixel_apply1(const Coef1& co, float2 L, float2
                        __saturatef(__fmaf_rn(co.A2, SB, __fmaf_rn(co.Bc, SF, co.qI))));
 }
 
+// ---- packed (F, B) form: Blackwell's fp32x2 FMA ------------------------------
+// Every operation of pixel_coef1_dl / pixel_apply1 is mirrored in (F, B) and
+// (u0, u1), so the pairs map onto sm_100's packed fp32 instructions (FFMA2 /
+// FMUL2 / FADD2: two IEEE fp32 results per issue slot, with free operand
+// broadcast, swap, negation and abs).  Each lane of a pair computes exactly
+// the scalar operation of the unpacked form, so results are bitwise equal to
+// pixel_coef1_dl + pixel_apply1 (the kernels' cross-check relies on it).  The
+// clamp is the one step without a packed form (no .sat on FFMA2): a separate
+// saturate per half.  The pre-clamp value is never -0 (A*SF >= +0 and the
+// inner term >= +0, see pixel_coef1), so saturate(x) equals FFMA.SAT's.
+typedef unsigned long long f32x2;
+
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(f32x2 v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ f32x2 pk2(float2 v) { return pk2(v.x, v.y); }
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// bilerp of two planes at once (same taps): bitwise equal to two bilerp calls.
+__device__ __forceinline__ float2 bilerp2(float2 a, float2 b, float2 c, float2 d, float tx, float ty) {
+    const f32x2 tx2 = pk2(tx, tx);
+    const f32x2 top = fma2(tx2, add2(pk2(b), pk2(-a.x, -a.y)), pk2(a));
+    const f32x2 bot = fma2(tx2, add2(pk2(d), pk2(-c.x, -c.y)), pk2(c));
+    const float2 tp = upk2(top);
+    const float2 r = upk2(fma2(pk2(ty, ty), add2(bot, pk2(-tp.x, -tp.y)), top));
+    return make_float2(__saturatef(r.x), __saturatef(r.y));
+}
+
+// Coef1 with (A, A2) and (pI, qI) as pairs and Bn = -Bc (negated for free as
+// a broadcast operand).
+struct CoefP {
+    float dL, dR, dU, dD, Bn;
+    float2 AA, PQ;
+};
+
+__device__ __forceinline__ CoefP pixel_coefp_dl(float a, float dL, float aR, float aU, float aD, float I, float eps,
+                                                float omega) {
+    CoefP co;
+    co.dL = dL;
+    {  // (dR, dU) = eps + omega |a - (aR, aU)|
+        const float2 df = upk2(add2(pk2(a, a), pk2(-aR, -aU)));
+        const float2 d = upk2(fma2(pk2(omega, omega), pk2(fabsf(df.x), fabsf(df.y)), pk2(eps, eps)));
+        co.dR = d.x;
+        co.dU = d.y;
+    }
+    co.dD = edge_weight(a, aD, eps, omega);
+    const float S = __fadd_rn(__fadd_rn(__fadd_rn(co.dL, co.dR), co.dU), co.dD);
+    const float u1 = __fsub_rn(1.0f, a);
+    const f32x2 u = pk2(a, u1);
+    const float2 uu = upk2(mul2(u, u));  // (u00, u11)
+    const float u01 = __fmul_rn(a, u1);
+    const float iS = rcp_approx(S);
+    const float iD = rcp_approx(__fadd_rn(__fadd_rn(uu.x, uu.y), S));
+    const f32x2 iD2 = pk2(iD, iD);
+    co.AA = upk2(mul2(iD2, fma2(pk2(uu.y, uu.x), pk2(iS, iS), pk2(1.0f, 1.0f))));
+    co.Bn = __fmul_rn(iD, __fmul_rn(u01, iS));
+    co.PQ = upk2(mul2(mul2(iD2, u), pk2(I, I)));
+    return co;
+}
+
+__device__ __forceinline__ float2 pixel_applyp(const CoefP& co, float2 L, float2 R, float2 U, float2 D) {
+    f32x2 s = mul2(pk2(co.dL, co.dL), pk2(L));
+    s = fma2(pk2(co.dD, co.dD), pk2(D), s);
+    s = fma2(pk2(co.dR, co.dR), pk2(R), s);
+    s = fma2(pk2(co.dU, co.dU), pk2(U), s);
+    const float2 sv = upk2(s);
+    const f32x2 t = fma2(pk2(-co.Bn, -co.Bn), pk2(sv.y, sv.x), pk2(co.PQ));
+    const float2 r = upk2(fma2(pk2(co.AA), s, t));
+    return make_float2(__saturatef(r.x), __saturatef(r.y));
+}
+
 // Neighbour-dependent part.  Values from this lane's previous step (L, D)
 // enter first, shuffled ones (R, U) last, to keep the recurrence short.
 __device__ __forceinline__ void pixel_apply(const Coef& co, const float* L, const float* R, const float* U,

@@ -136,22 +136,36 @@ __global__ void __launch_bounds__(kResCols) resample_kernel(const ResampleJob* _
 #ifndef FGM_UP_ROWS
 #define FGM_UP_ROWS 8
 #endif
-constexpr int kUpCols = 128, kUpRows = FGM_UP_ROWS, kUpThreads = 128;
+#ifndef FGM_UP_THREADS
+#define FGM_UP_THREADS 128
+#endif
+constexpr int kUpCols = 128, kUpRows = FGM_UP_ROWS, kUpThreads = FGM_UP_THREADS, kUpWarps = kUpThreads / 32;
+static_assert(kUpRows % kUpWarps == 0, "every warp takes the same number of tile rows");
 constexpr double kUpMaxScale = 0.625;
 constexpr int kUpSR = (kUpRows - 1) * 5 / 8 + 4;  // >= ceil((rows-1) * 0.625) + 3
-constexpr int kUpSC = 83;  // ceil(127 * 0.625) + 3
+// window columns: ceil(127 * 0.625) + 3 = 83, plus up to 3 + 3 for the
+// 16-byte block alignment of both ends, rounded to 16 bytes
+constexpr int kUpSC = 92;
 constexpr int kUpPlane = kUpSR * kUpSC;
 constexpr int kUpBuf = 6 * kUpPlane;
 
 __device__ __forceinline__ void cp_async_f32(unsigned sdst, const float* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sdst), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async_v4(unsigned sdst, const float* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void st_cs(float* p, float v) {
+    asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
 
 struct UpTile {
-    int job, y0, x0, nrows, ncols, r0, c0, nr, nc;  // nr x nc: staged source window
+    int job, y0, x0, nrows, ncols, r0, c0, nr, nc;  // nr x nc: staged source window from (r0, c0)
 };
 
 // Tile geometry and source window; `job` advances monotonically per block.
+// With 16-byte staging (v4) the window starts at the 4-aligned column below
+// the first tap.
 __device__ __forceinline__ UpTile up_tile(const ResampleJob* __restrict__ jobs, int njobs, int gt, int job) {
     while (job + 1 < njobs && jobs[job + 1].tile_base <= gt) ++job;
     const ResampleJob& J = jobs[job];
@@ -165,27 +179,46 @@ __device__ __forceinline__ UpTile up_tile(const ResampleJob* __restrict__ jobs, 
     t.nrows = min(kUpRows, J.dh - t.y0);
     t.ncols = min(kUpCols, J.dw - t.x0);
     t.r0 = make_tap_s(t.y0, J.sh, J.sy).i0;
-    t.c0 = make_tap_s(t.x0, J.sw, J.sx).i0;
+    const int c0 = make_tap_s(t.x0, J.sw, J.sx).i0;
     // exact window: up to the last row's / column's i1
     t.nr = make_tap_s(t.y0 + t.nrows - 1, J.sh, J.sy).i1 - t.r0 + 1;
-    t.nc = make_tap_s(t.x0 + t.ncols - 1, J.sw, J.sx).i1 - t.c0 + 1;
+    const int c1 = make_tap_s(t.x0 + t.ncols - 1, J.sw, J.sx).i1;
+    const bool v4 = ((reinterpret_cast<uintptr_t>(J.src) | uintptr_t(J.spitch) | uintptr_t(J.spstride)) & 3) == 0 &&
+                    (reinterpret_cast<uintptr_t>(J.src) & 15) == 0;
+    t.c0 = v4 ? (c0 & ~3) : c0;
+    t.nc = v4 ? -(((c1 | 3) - t.c0 + 1) >> 2) : c1 - c0 + 1;  // < 0: number of 16-byte blocks
     return t;
 }
 
-// Issue the cp.async loads of a tile's window (rows r0.., columns c0..,
-// clamped to the source) and its row taps (threads 0..7) into buffer b.
+// Issue the cp.async loads of a tile's window and its row taps (threads
+// 0..7) into buffer b.  16-byte blocks when the source rows allow it (level
+// buffers are pitched to 4 floats; the blocks may read into the row padding,
+// which no tap uses).
 __device__ __forceinline__ void up_stage(const ResampleJob& J, const UpTile& t, unsigned sbuf, Tap* tys, int tid) {
-    const int nr = t.nr, nc = t.nc;  // <= kUpSR x kUpSC at scales <= kUpMaxScale
+    const int nr = t.nr;  // <= kUpSR at scales <= kUpMaxScale
     const int sp = J.spitch;
     const long long sps = J.spstride;
     const int warp = tid >> 5, lane = tid & 31;
+    if (t.nc < 0) {
+        const int nb = -t.nc;  // blocks per row (<= kUpSC / 4 = 23 < 32: one per lane)
 #pragma unroll
-    for (int p = 0; p < 6; ++p) {
-        const float* sp0 = J.src + p * sps + (long long)t.r0 * sp + t.c0;
-        for (int r = warp; r < nr; r += kUpThreads / 32) {
-            const float* srow = sp0 + (long long)r * sp;
-            const unsigned drow = sbuf + 4u * unsigned(p * kUpPlane + r * kUpSC);
-            for (int c = lane; c < nc; c += 32) cp_async_f32(drow + 4u * c, srow + c);
+        for (int p = 0; p < 6; ++p) {
+            const float* sp0 = J.src + p * sps + (long long)t.r0 * sp + t.c0 + 4 * lane;
+            const unsigned d0 = sbuf + 4u * unsigned(p * kUpPlane + 4 * lane);
+            if (lane < nb)
+                for (int r = warp; r < nr; r += kUpThreads / 32)
+                    cp_async_v4(d0 + 4u * unsigned(r * kUpSC), sp0 + (long long)r * sp);
+        }
+    } else {
+        const int nc = t.nc;
+#pragma unroll
+        for (int p = 0; p < 6; ++p) {
+            const float* sp0 = J.src + p * sps + (long long)t.r0 * sp + t.c0;
+            for (int r = warp; r < nr; r += kUpThreads / 32) {
+                const float* srow = sp0 + (long long)r * sp;
+                const unsigned drow = sbuf + 4u * unsigned(p * kUpPlane + r * kUpSC);
+                for (int c = lane; c < nc; c += 32) cp_async_f32(drow + 4u * c, srow + c);
+            }
         }
     }
     if (tid < t.nrows) tys[tid] = make_tap_s(t.y0 + tid, J.sh, J.sy);
@@ -216,38 +249,49 @@ __global__ void __launch_bounds__(kUpThreads) upsample_kernel(const ResampleJob*
         {
             // thread = (lane l, warp rp): columns x0 + l + 32i (i < 4), rows
             // rp, rp + 4, ...  Lanes read neighbouring (or equal) staged words:
-            // no bank conflicts; stores are 128-byte warp rows.
+            // no bank conflicts; stores are 128-byte warp rows.  Columns past
+            // the tile's end are computed on a clamped column and not stored.
             const ResampleJob& J = jobs[cur.job];
             const int l = tid & 31, rp = tid >> 5;
-            int sa[4], dx[4];
+            int ca[4], cb[4];
             float tx[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const Tap t = make_tap_s(min(cur.x0 + l + 32 * i, J.dw - 1), J.sw, J.sx);
-                sa[i] = t.i0 - cur.c0;
-                dx[i] = t.i1 - t.i0;
+                ca[i] = t.i0 - cur.c0;
+                cb[i] = t.i1 - cur.c0;
                 tx[i] = t.t;
             }
             const float* buf = sm + b * kUpBuf;
             const long long dps = J.dpstride;
+            float* dcol = J.dst + cur.x0 + l;
 #pragma unroll
-            for (int h = 0; h < kUpRows / 4; ++h) {
-                const int rr = rp + 4 * h;
+            for (int h = 0; h < kUpRows / kUpWarps; ++h) {
+                const int rr = rp + kUpWarps * h;  // warp-uniform
                 if (rr >= cur.nrows) break;
                 const Tap ty = tys[b][rr];
                 const float* ra = buf + (ty.i0 - cur.r0) * kUpSC;
                 const float* rc = buf + (ty.i1 - cur.r0) * kUpSC;
-                float* d = J.dst + (long long)(cur.y0 + rr) * J.dpitch + cur.x0 + l;
+                float* d = dcol + (long long)(cur.y0 + rr) * J.dpitch;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    if (l + 32 * i >= cur.ncols) break;
+                    if (l + 32 * i >= cur.ncols) break;  // (the tile's last column block only)
+                    const float* a0 = ra + ca[i];
+                    const float* a1 = ra + cb[i];
+                    const float* c0 = rc + ca[i];
+                    const float* c1 = rc + cb[i];
+                    float v[6];
 #pragma unroll
-                    for (int p = 0; p < 6; ++p) {
-                        const float* a = ra + p * kUpPlane + sa[i];
-                        const float* c = rc + p * kUpPlane + sa[i];
-                        // streaming store: the next level's sweep reads it once, much later
-                        __stcs(d + p * dps + 32 * i, bilerp(a[0], a[dx[i]], c[0], c[dx[i]], tx[i], ty.t));
+                    for (int p = 0; p < 6; p += 2) {  // plane pairs: packed fp32x2 arithmetic
+                        const int o = p * kUpPlane, q = o + kUpPlane;
+                        const float2 r = bilerp2(make_float2(a0[o], a0[q]), make_float2(a1[o], a1[q]),
+                                                 make_float2(c0[o], c0[q]), make_float2(c1[o], c1[q]), tx[i], ty.t);
+                        v[p] = r.x;
+                        v[p + 1] = r.y;
                     }
+                    // streaming stores: the next level's sweep reads them once, much later
+#pragma unroll
+                    for (int p = 0; p < 6; ++p) st_cs(d + p * dps + 32 * i, v[p]);
                 }
             }
         }

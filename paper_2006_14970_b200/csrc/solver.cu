@@ -103,8 +103,8 @@ struct ProfRec {
 std::mutex g_prof_mu;
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
-long long g_launches[3] = {0, 0, 0};
-double g_ms[3] = {0, 0, 0}, g_bytes[3] = {0, 0, 0};
+long long g_launches[4] = {0, 0, 0, 0};  // sweep, resample (I/alpha pyramid), coarse, upsample (F/B)
+double g_ms[4] = {0, 0, 0, 0}, g_bytes[4] = {0, 0, 0, 0};
 
 // Events come from a free list (created once, reused after each drain) so
 // that profiling adds no host-side event creation to the timed launches.
@@ -143,15 +143,29 @@ struct ProfScope {
     }
 };
 
+// Timeline of the last drained launches (kind, start, end in ms from the
+// first recorded launch), for fgm_profile_timeline.
+struct TimeRec {
+    int which;
+    double t0, t1;
+};
+std::vector<TimeRec> g_timeline;
+
 void prof_drain() {
     std::lock_guard<std::mutex> g(g_prof_mu);
+    if (!g_prof.empty()) g_timeline.clear();
     for (auto& r : g_prof) {
         cudaEventSynchronize(r.b);
-        float ms = 0;
+        float ms = 0, t0 = 0, t1 = 0;
         cudaEventElapsedTime(&ms, r.a, r.b);
+        cudaEventElapsedTime(&t0, g_prof.front().a, r.a);
+        cudaEventElapsedTime(&t1, g_prof.front().a, r.b);
+        g_timeline.push_back({r.which, t0, t1});
         g_launches[r.which] += 1;
         g_ms[r.which] += ms;
         g_bytes[r.which] += r.bytes;
+    }
+    for (auto& r : g_prof) {
         g_ev_free.push_back(r.a);
         g_ev_free.push_back(r.b);
     }
@@ -724,7 +738,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 break;
             }
             case kUpsample: {
-                ProfScope ps(s, 1, r.bytes);
+                ProfScope ps(s, 3, r.bytes);
                 ck(launch_upsample(reinterpret_cast<const ResampleJob*>(djobs + r.job_off), r.njobs, r.max_rows, s),
                    "upsample_kernel");
                 break;
@@ -1174,7 +1188,7 @@ void fgm_profile_enable(int on) {
 void fgm_profile_reset(void) {
     prof_drain();
     std::lock_guard<std::mutex> g(g_prof_mu);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 4; ++i) {
         g_launches[i] = 0;
         g_ms[i] = 0;
         g_bytes[i] = 0;
@@ -1182,13 +1196,25 @@ void fgm_profile_reset(void) {
 }
 
 int fgm_kernel_stats(int which, long long* launches, double* ms, double* alg_bytes) {
-    if (which < 0 || which > 2) return FGM_INVALID_ARGUMENT;
+    if (which < 0 || which > 3) return FGM_INVALID_ARGUMENT;
     prof_drain();
     std::lock_guard<std::mutex> g(g_prof_mu);
     if (launches) *launches = g_launches[which];
     if (ms) *ms = g_ms[which];
     if (alg_bytes) *alg_bytes = g_bytes[which];
     return FGM_OK;
+}
+
+int fgm_profile_timeline(int max, int* which, double* t0, double* t1) {
+    prof_drain();
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    const int n = int(g_timeline.size());
+    for (int i = 0; i < std::min(n, max); ++i) {
+        if (which) which[i] = g_timeline[size_t(i)].which;
+        if (t0) t0[i] = g_timeline[size_t(i)].t0;
+        if (t1) t1[i] = g_timeline[size_t(i)].t1;
+    }
+    return n;
 }
 
 const char* fgm_last_error(void) { return fgm::g_err.c_str(); }

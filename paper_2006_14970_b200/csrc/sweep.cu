@@ -244,6 +244,31 @@ __device__ __forceinline__ void prologue_row(const RowSrc& rs, int t0, int w) {
     for (int x0 = 0; x0 <= last; x0 += 4) put_blocks<K, V4>(rs, x0, w);
 }
 
+// Packed (F, B) arithmetic (FFMA2, fgm_device.cuh) or the scalar form; the
+// two are bitwise identical.
+#ifndef FGM_PACKED
+#define FGM_PACKED 1
+#endif
+#if FGM_PACKED
+using SCoef = CoefP;
+__device__ __forceinline__ SCoef coef_dl(float a, float dL, float aR, float aU, float aD, float I, float eps,
+                                         float omega) {
+    return pixel_coefp_dl(a, dL, aR, aU, aD, I, eps, omega);
+}
+__device__ __forceinline__ float2 apply_coef(const SCoef& co, float2 L, float2 R, float2 U, float2 D) {
+    return pixel_applyp(co, L, R, U, D);
+}
+#else
+using SCoef = Coef1;
+__device__ __forceinline__ SCoef coef_dl(float a, float dL, float aR, float aU, float aD, float I, float eps,
+                                         float omega) {
+    return pixel_coef1_dl(a, dL, aR, aU, aD, I, eps, omega);
+}
+__device__ __forceinline__ float2 apply_coef(const SCoef& co, float2 L, float2 R, float2 U, float2 D) {
+    return pixel_apply1(co, L, R, U, D);
+}
+#endif
+
 // Float offset, from rc = lane_base + c, of ring `off`, ring row lane + row,
 // shifted column offset dp.
 template <int K>
@@ -255,7 +280,7 @@ __device__ __forceinline__ constexpr int ring(int off, int row, int dp) {
 // t - lane), its left edge weight `dL` given.  G: clamp neighbours at the
 // image border.
 template <int K, bool G, bool Y = false, bool XL = false>
-__device__ __forceinline__ Coef1 next_coef(int rc, int k, float dL, int x, int y, int w, int h, float eps,
+__device__ __forceinline__ SCoef next_coef(int rc, int k, float dL, int x, int y, int w, int h, float eps,
                                            float omega) {
     using Gm = Geom<K>;
     const int dp = 1 - k + Gm::SH;  // shifted column of the pixel
@@ -275,12 +300,12 @@ __device__ __forceinline__ Coef1 next_coef(int rc, int k, float dL, int x, int y
         if (y <= 0) aU = a;
         if (y >= h - 1) aD = a;
     }
-    return pixel_coef1_dl(a, dL, aR, aU, aD, I, eps, omega);
+    return coef_dl(a, dL, aR, aU, aD, I, eps, omega);
 }
 
 // Coefficients from scratch (the first step of a band: no left pixel yet).
 template <int K>
-__device__ __forceinline__ Coef1 first_coef(int rc, int k, int x, int y, int w, int h, float eps, float omega) {
+__device__ __forceinline__ SCoef first_coef(int rc, int k, int x, int y, int w, int h, float eps, float omega) {
     using Gm = Geom<K>;
     const int dp = 1 - k + Gm::SH;
     const int ar = K - k;
@@ -294,7 +319,7 @@ template <int K>
 struct LaneState {
     float2 outp[K];   // this lane's (F_c, B_c) outputs of the previous step
     float2 rprev[K];  // what this lane received from lane-1 at the previous step (border steps)
-    Coef1 co[K];      // coefficients of this step's pixels (computed one step ahead)
+    SCoef co[K];      // coefficients of this step's pixels (computed one step ahead)
 };
 
 template <int K>
@@ -368,7 +393,7 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
                 if (!(y < h - 1)) D = self;
             }
         }
-        nv[k] = pixel_apply1(st.co[k], L, R, U, D);
+        nv[k] = apply_coef(st.co[k], L, R, U, D);
     }
 
     // coefficients of the next step's pixels; dL = this step's dR of the slot

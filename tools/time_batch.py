@@ -25,7 +25,7 @@ for _ in range(3):
         fgm.batch_solve_cuda(imgs, alps, fgm.BASELINE_PARAMS, outputs=outs)
         torch.cuda.synchronize()
     st = fgm.profile.stats()
-    res.append((st["sweep"]["ms"], st["resample"]["ms"]))
+    res.append((st["sweep"]["ms"], st["resample"]["ms"], st["upsample"]["ms"]))
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(3):
@@ -34,4 +34,4 @@ e1.record()
 torch.cuda.synchronize()
 lib = os.environ.get("FGMATTE_B200_LIB", "default")
 print(f"{lib}: mode {mode} total {e0.elapsed_time(e1) / 3:.2f} ms  sweep {min(r[0] for r in res):.2f} ms  "
-      f"resample {min(r[1] for r in res):.2f} ms", flush=True)
+      f"resample {min(r[1] for r in res):.2f} ms  upsample {min(r[2] for r in res):.2f} ms", flush=True)
