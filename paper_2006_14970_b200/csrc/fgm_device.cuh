@@ -279,6 +279,61 @@ __device__ __forceinline__ float2 pixel_applyp(const CoefP& co, float2 L, float2
     return make_float2(__saturatef(r.x), __saturatef(r.y));
 }
 
+// ---- rank-one form (the K3 default) -----------------------------------------
+// The matrix is M = S I + u u^T (multilevel.hpp:37-43: a00 = u0^2 + S,
+// a01 = u0 u1, a11 = u1^2 + S), so by Sherman-Morrison
+//   M^-1 = (I - u u^T / D) / S,   D = |u|^2 + S,
+// and with b = I_c u + (SF_c, SB_c), Fbar = SF_c / S, Bbar = SB_c / S:
+//   (F_c, B_c) = (Fbar, Bbar) + (u0, u1) / D * (I_c - u0 Fbar - u1 Bbar).
+// The same solution as the reference's adj(M) b / det(M) (det = S D), with no
+// cancellation beyond the data's own: Fbar is a convex combination of the
+// neighbours, the residual I_c - u.(Fbar, Bbar) is bounded by 1 and its
+// rounding error is scaled by u0 / D <= 1.  Per pixel: 11 alpha-only
+// operations + 2 reciprocals (edge weights, S, D, u/D) and 11 per channel
+// (the weighted sums, the residual and the update); the old A/A2/Bc form
+// needs ~22 + 8.  Every operation is mirrored in (F, B) / (u0, u1) or is a
+// commutative sum of the two halves, so complementing alpha swaps F and B
+// bitwise (test_multilevel.cpp:167-180).
+struct CoefR {
+    float dL, dR, dU, dD, iS, I;
+    f32x2 u;   // (a, 1 - a)
+    f32x2 pq;  // u / D
+};
+
+__device__ __forceinline__ CoefR pixel_coefr_dl(float a, float dL, float aR, float aU, float aD, float I, float eps,
+                                                float omega) {
+    CoefR co;
+    co.dL = dL;
+    {  // (dR, dU) = eps + omega |a - (aR, aU)|
+        const float2 df = upk2(add2(pk2(a, a), pk2(-aR, -aU)));
+        const float2 d = upk2(fma2(pk2(omega, omega), pk2(fabsf(df.x), fabsf(df.y)), pk2(eps, eps)));
+        co.dR = d.x;
+        co.dU = d.y;
+    }
+    co.dD = edge_weight(a, aD, eps, omega);
+    const float S = __fadd_rn(__fadd_rn(__fadd_rn(co.dL, co.dR), co.dU), co.dD);
+    co.u = pk2(a, __fsub_rn(1.0f, a));
+    const float2 uu = upk2(mul2(co.u, co.u));
+    const float Dn = __fadd_rn(__fadd_rn(uu.x, uu.y), S);
+    co.iS = rcp_approx(S);
+    const float iD = rcp_approx(Dn);
+    co.pq = mul2(pk2(iD, iD), co.u);
+    co.I = I;
+    return co;
+}
+
+__device__ __forceinline__ float2 pixel_applyr(const CoefR& co, float2 L, float2 R, float2 U, float2 D) {
+    f32x2 s = mul2(pk2(co.dL, co.dL), pk2(L));
+    s = fma2(pk2(co.dD, co.dD), pk2(D), s);
+    s = fma2(pk2(co.dR, co.dR), pk2(R), s);
+    s = fma2(pk2(co.dU, co.dU), pk2(U), s);
+    const f32x2 m = mul2(pk2(co.iS, co.iS), s);  // (Fbar, Bbar)
+    const float2 t = upk2(mul2(co.u, m));  // (u0 Fbar, u1 Bbar)
+    const float r = __fsub_rn(co.I, __fadd_rn(t.x, t.y));
+    const float2 o = upk2(fma2(co.pq, pk2(r, r), m));
+    return make_float2(__saturatef(o.x), __saturatef(o.y));
+}
+
 // Neighbour-dependent part.  Values from this lane's previous step (L, D)
 // enter first, shuffled ones (R, U) last, to keep the recurrence short.
 __device__ __forceinline__ void pixel_apply(const Coef& co, const float* L, const float* R, const float* U,

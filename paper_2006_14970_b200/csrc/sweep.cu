@@ -247,9 +247,18 @@ __device__ __forceinline__ void prologue_row(const RowSrc& rs, int t0, int w) {
 // Packed (F, B) arithmetic (FFMA2, fgm_device.cuh) or the scalar form; the
 // two are bitwise identical.
 #ifndef FGM_PACKED
-#define FGM_PACKED 1
+#define FGM_PACKED 2
 #endif
-#if FGM_PACKED
+#if FGM_PACKED == 2
+using SCoef = CoefR;
+__device__ __forceinline__ SCoef coef_dl(float a, float dL, float aR, float aU, float aD, float I, float eps,
+                                         float omega) {
+    return pixel_coefr_dl(a, dL, aR, aU, aD, I, eps, omega);
+}
+__device__ __forceinline__ float2 apply_coef(const SCoef& co, float2 L, float2 R, float2 U, float2 D) {
+    return pixel_applyr(co, L, R, U, D);
+}
+#elif FGM_PACKED
 using SCoef = CoefP;
 __device__ __forceinline__ SCoef coef_dl(float a, float dL, float aR, float aU, float aD, float I, float eps,
                                          float omega) {

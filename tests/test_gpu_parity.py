@@ -376,8 +376,10 @@ def test_batch_equals_single_bitwise(fgm, cuda):
 
 @pytest.mark.parametrize("kw", [dict(), dict(iters_high=1), dict(iters_high=3), dict(iters_high=5)])
 def test_sweep_kernels_agree_bitwise(fgm, cuda, oracle_mod, kw):
-    # per-(band, channel) warps vs full-channel warps with passed coefficients:
-    # the same arithmetic, so the same bits
+    # the two experimental K3 variants (full-channel warps with passed
+    # coefficients; band CTAs with a coefficient warp) run the same A/A2/Bc
+    # arithmetic, so the same bits; the default kernel (rank-one form) agrees
+    # with them within the oracle tolerance
     from paper_2006_14970_b200 import synth
 
     p = params_from(fgm, oracle_mod.Params(**kw))
@@ -395,9 +397,13 @@ def test_sweep_kernels_agree_bitwise(fgm, cuda, oracle_mod, kw):
         c = fgm.batch_solve_cuda(imgs, alps, p)
     finally:
         fgm.set_sweep_mode(0)
+    # (the band-CTA kernel exists for K <= 2; K = 3 passes fall back to the default kernel)
+    cta_everywhere = kw.get("iters_high", 2) in (1, 2)
     for (fa, ba), (fb, bb), (fc, bc) in zip(a, b, c):
-        assert torch.equal(fa, fb) and torch.equal(ba, bb)
-        assert torch.equal(fa, fc) and torch.equal(ba, bc)
+        if cta_everywhere:
+            assert torch.equal(fb, fc) and torch.equal(bb, bc)
+        for x, y in ((fa, fb), (ba, bb), (fa, fc), (ba, bc)):
+            assert (x - y).abs().max().item() <= TOL_MAX
 
 
 def test_full_channel_kernel_vs_oracle(fgm, cuda, orc, oracle_mod):
