@@ -99,24 +99,31 @@ __device__ __forceinline__ void sts(int i, float v) { smf()[i] = v; }
 __device__ __forceinline__ void sts4(int i, float4 v) { reinterpret_cast<float4*>(smf() + i)[0] = v; }
 __device__ __forceinline__ void stg(float* p, float v) { __stcg(p, v); }
 __device__ __forceinline__ bool is_sentinel(float v) { return __float_as_uint(v) == kStreamSentinel; }
-
+#ifndef FGM_GROUP
+#define FGM_GROUP 4
+#endif
 // Shared-memory geometry of one (band, channel) warp, in floats.
 //
 // Ring window.  In row-time tau = x + r (band row r, column x) the reads of
 // step t cover alpha tau in [t-2K+2, t+2] (the next step's pixels and their
-// four neighbours), image [t-2K+3, t+1] and the initial F/B [t, t+1].  Loads
-// of 4-column blocks are issued at the end of each 4-step group with a lead
-// L = 4M - 1 + W1 (W1 = the window's reach past the group), so a group waits
-// only for loads issued M groups earlier; the live span 4M + 3 + W0 + W1 must
-// fit in the 32 ring columns (static_asserts below).
+// four neighbours), image [t-2K+3, t+1] and the initial F/B [t, t+1].  Steps
+// run in groups of S = 4; the S-column blocks of every row are issued at
+// the end of each group with a lead L = S*M - 1 + W1 (W1 = the window's reach
+// past the group), so a group waits only for loads issued M groups earlier;
+// the live span S*M + S - 1 + W0 + W1 must fit in the 32 ring columns
+// (static_asserts below).
 template <int K, int CK = kChunk>
 struct Geom {
     static constexpr int RW = 32;               // ring columns
     static constexpr int SH = K - 1;            // read column shift: offsets d + SH >= 0
     static constexpr int MIR = K <= 2 ? 4 : 8;  // mirrored columns (> largest shifted offset)
     static constexpr int RS = RW + MIR;         // row stride (floats), 16-byte multiple, RS - 1 odd
-    static constexpr int M = 4;                 // load groups in flight
-    static constexpr int L = 4 * M + 1;         // load lead: 4M - 1 + W1, W1 = 2 (alpha; 1 for the others)
+    // steps per group = columns per load block.  (8 in throughput launches
+    // runs 2% fewer instructions but measured 3% slower on the C4 batch: the
+    // four unrolled 8-step paths no longer share the instruction cache.)
+    static constexpr int S = FGM_GROUP;
+    static constexpr int M = 16 / S;            // load groups in flight
+    static constexpr int L = S * M + 1;         // load lead: S*M - 1 + W1, W1 = 2 (alpha; 1 for the others)
     static constexpr int NA = 33 + K;           // alpha ring rows: band rows -K .. 32
     static constexpr int NI = 31 + K;           // image ring rows: band rows -(K-1) .. 31
     static constexpr int NF = 33;               // F/B ring rows: band rows 0 .. 32
@@ -131,7 +138,7 @@ struct Geom {
     static constexpr int CH = CK * K * 2;      // one boundary-stream chunk of CK columns: [u][k][F,B]
     static constexpr int CH4 = CH / 4;         // float4 per chunk (<= 32: one per lane)
     static constexpr int TOTAL = OFF_C + CH;
-    static_assert(L + (2 * K - 2) + 4 <= RW, "alpha ring too small for its lead");
+    static_assert(L + (2 * K - 2) + S <= RW, "alpha ring too small for its lead");
     static_assert(2 + SH <= MIR && MIR % 4 == 0 && RS % 4 == 0, "mirror too narrow");
     static_assert(CH % 4 == 0 && CH4 <= 32, "a chunk is at most one float4 per lane");
 };
@@ -178,70 +185,80 @@ __device__ __forceinline__ constexpr int plane_off(int p) {
     return p == 0 ? G::OFF_A + K * G::RS : p == 1 ? G::OFF_I + (K - 1) * G::RS : p == 2 ? G::OFF_F : G::OFF_B;
 }
 
-// cp.async of the 4-column block at column x0 of every streamed plane of one
-// row into the rings (and into the mirror columns when it lands in the first
-// MIR columns).  Columns past the row end are zero-filled (src-size); blocks
-// outside [0, w) are skipped.
-template <int K, bool V4>
+// cp.async of the S-column block at column x0 (S-aligned) of every streamed
+// plane of one row into the rings, as 4-column pieces (each also into the
+// mirror columns when it lands in the first MIR columns).  Columns past the
+// row end are zero-filled (src-size); pieces outside [0, w) are skipped.
+template <int K, bool V4, int CK>
 __device__ __forceinline__ void put_blocks(const RowSrc& rs, int x0, int w) {
-    using G = Geom<K>;
-    if (x0 < 0 || x0 >= w) return;
-    const int nb = min(w - x0, 4) * 4;
-    const int c = x0 & (G::RW - 1);
-    const unsigned sc = rs.s + 4u * c;
-    const bool mir = c < G::MIR;
+    using G = Geom<K, CK>;
+    if (x0 < 0) return;
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        if (!(rs.vm & (1u << p))) continue;
-        const float* g = rs.g[p] + x0;
-        const unsigned d = sc + 4u * plane_off<K>(p);
-        if (V4) {
-            cp_async16(d, g, nb);
-            if (mir) cp_async16(d + 4u * G::RW, g, nb);
-        } else {
+    for (int b = 0; b < G::S / 4; ++b) {
+        const int xb = x0 + 4 * b;
+        if (xb >= w) return;
+        const int nb = min(w - xb, 4) * 4;
+        const int c = xb & (G::RW - 1);
+        const unsigned sc = rs.s + 4u * c;
+        const bool mir = c < G::MIR;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int ok = 4 * i < nb;
-                cp_async4(d + 4 * i, ok ? g + i : g, ok ? 4 : 0);
-                if (mir) cp_async4(d + 4u * G::RW + 4 * i, ok ? g + i : g, ok ? 4 : 0);
+        for (int p = 0; p < 4; ++p) {
+            if (!(rs.vm & (1u << p))) continue;
+            const float* g = rs.g[p] + xb;
+            const unsigned d = sc + 4u * plane_off<K>(p);
+            if (V4) {
+                cp_async16(d, g, nb);
+                if (mir) cp_async16(d + 4u * G::RW, g, nb);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int ok = 4 * i < nb;
+                    cp_async4(d + 4 * i, ok ? g + i : g, ok ? 4 : 0);
+                    if (mir) cp_async4(d + 4u * G::RW + 4 * i, ok ? g + i : g, ok ? 4 : 0);
+                }
             }
         }
     }
 }
 
-// The blocks of one row issued at the end of group t4 (lead L).
-template <int K, bool V4>
+// The block of one row issued at the end of group t4 (lead L).
+template <int K, bool V4, int CK>
 __device__ __forceinline__ void issue_row(const RowSrc& rs, int t4, int w) {
-    put_blocks<K, V4>(rs, (t4 + 4 + Geom<K>::L - rs.r) & ~3, w);
+    using G = Geom<K, CK>;
+    put_blocks<K, V4, CK>(rs, (t4 + G::S + G::L - rs.r) & ~(G::S - 1), w);
 }
 
 // Interior groups of 16-byte-aligned jobs: every lane's block is inside
 // [0, w), so no range checks and no zero-fill; the per-lane plane mask and
 // the mirror copy become instruction predicates.  MASK: compile-time plane
 // mask (15 for a lane's own row of an interior band), else rs.vm.
-template <int K, unsigned MASK>
+template <int K, unsigned MASK, int CK>
 __device__ __forceinline__ void issue_row_fast(const RowSrc& rs, int t4) {
-    using G = Geom<K>;
-    const unsigned x0 = unsigned(t4 + 4 + G::L - rs.r) & ~3u;  // >= 0 in interior groups
-    const unsigned c = x0 & (G::RW - 1);
+    using G = Geom<K, CK>;
+    const unsigned x0 = unsigned(t4 + G::S + G::L - rs.r) & ~unsigned(G::S - 1);  // >= 0 in interior groups
+    const unsigned c = x0 & (G::RW - 1);  // S-aligned: the pieces of a block never wrap the ring
     const unsigned sc = rs.s + 4u * c;
-    const unsigned mir = c < unsigned(G::MIR) ? 1u : 0u;
     const unsigned vm = MASK ? MASK : rs.vm;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const float* g = rs.g[p] + x0;
         const unsigned d = sc + 4u * plane_off<K>(p);
         const unsigned on = (vm >> p) & 1u;
-        cp_async16_if(d, g, on);
-        cp_async16_if(d + 4u * G::RW, g, on & mir);
+#pragma unroll
+        for (int b = 0; b < G::S / 4; ++b) {
+            cp_async16_if(d + 16u * b, g + 4 * b, on);
+            if (4 * b < G::MIR)  // only the first MIR columns of the ring are mirrored
+                cp_async16_if(d + 16u * b + 4u * G::RW, g + 4 * b, on & (c + 4u * b < unsigned(G::MIR) ? 1u : 0u));
+        }
     }
 }
 
 // Everything issued "before group t0".
-template <int K, bool V4>
+template <int K, bool V4, int CK>
 __device__ __forceinline__ void prologue_row(const RowSrc& rs, int t0, int w) {
-    const int last = (t0 + Geom<K>::L - rs.r) & ~3;  // the block issued at the end of group t0 - 4
-    for (int x0 = 0; x0 <= last; x0 += 4) put_blocks<K, V4>(rs, x0, w);
+    using G = Geom<K, CK>;
+    const int last = (t0 + G::L - rs.r) & ~(G::S - 1);  // the block issued at the end of group t0 - S
+    for (int x0 = 0; x0 <= last; x0 += G::S) put_blocks<K, V4, CK>(rs, x0, w);
 }
 
 // Packed (F, B) arithmetic (FFMA2, fgm_device.cuh) or the scalar form; the
@@ -570,9 +587,10 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
 
     // prologue: the loads "issued before" the first group, then M-1 empty
     // groups so that every group waits with the same cp.async.wait_group M-1
-    constexpr int t0 = -4;
-    prologue_row<K, V4>(own, t0, w);
-    if (has_x) prologue_row<K, V4>(ext, t0, w);
+    constexpr int S = Gm::S;
+    constexpr int t0 = -S;
+    prologue_row<K, V4, CK>(own, t0, w);
+    if (has_x) prologue_row<K, V4, CK>(ext, t0, w);
     cp_commit();
 #pragma unroll
     for (int i = 1; i < Gm::M; ++i) cp_commit();
@@ -588,8 +606,8 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     const int fast_lo = 32 + K, fast_hi = w - 2;  // a step tr is fast iff fast_lo <= tr < fast_hi
     const int tend = 31 + Umax;                   // lane 31's last column is Umax-1
     // groups whose issued blocks are inside [0, w) for every row -K .. 32
-    const int issue_lo = 32 + 3 - 4 - Gm::L, issue_hi = w - 4 - 4 - Gm::L - K;
-    for (int t4 = t0; t4 < tend; t4 += 4) {
+    const int issue_lo = 32 - Gm::L, issue_hi = w - 2 * S - Gm::L - K;
+    for (int t4 = t0; t4 < tend; t4 += S) {
         cp_wait<Gm::M - 1>();
         __syncwarp();
         if (t4 < 0) {
@@ -617,32 +635,32 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
                 }
             }
             __syncwarp();
-            if (t4 >= fast_lo && t4 + 4 <= fast_hi && !yband) {
+            if (t4 >= fast_lo && t4 + S <= fast_hi && !yband) {
 #pragma unroll
-                for (int s = 0; s < 4; ++s) band_step<K, false, CK>(st, cx, t4 + s);
-            } else if (t4 >= fast_lo && t4 + 4 <= fast_hi) {
+                for (int s = 0; s < S; ++s) band_step<K, false, CK>(st, cx, t4 + s);
+            } else if (t4 >= fast_lo && t4 + S <= fast_hi) {
 #pragma unroll
-                for (int s = 0; s < 4; ++s) band_step<K, false, CK, true>(st, cx, t4 + s);
-            } else if (t4 < fast_lo && t4 + 4 <= fast_hi) {  // band start: left border only
+                for (int s = 0; s < S; ++s) band_step<K, false, CK, true>(st, cx, t4 + s);
+            } else if (t4 < fast_lo && t4 + S <= fast_hi) {  // band start: left border only
                 if (yband) {
 #pragma unroll
-                    for (int s = 0; s < 4; ++s) band_step<K, false, CK, true, true>(st, cx, t4 + s);
+                    for (int s = 0; s < S; ++s) band_step<K, false, CK, true, true>(st, cx, t4 + s);
                 } else {
 #pragma unroll
-                    for (int s = 0; s < 4; ++s) band_step<K, false, CK, false, true>(st, cx, t4 + s);
+                    for (int s = 0; s < S; ++s) band_step<K, false, CK, false, true>(st, cx, t4 + s);
                 }
             } else {
 #pragma unroll 1
-                for (int s = 0; s < 4; ++s) band_step<K, true, CK>(st, cx, t4 + s);
+                for (int s = 0; s < S; ++s) band_step<K, true, CK>(st, cx, t4 + s);
             }
         }
         __syncwarp();  // every lane is done with the ring slots the next loads overwrite
         if (V4 && !yband && t4 >= issue_lo && t4 < issue_hi) {
-            issue_row_fast<K, 15u>(own, t4);
-            issue_row_fast<K, 0u>(ext, t4);
+            issue_row_fast<K, 15u, CK>(own, t4);
+            issue_row_fast<K, 0u, CK>(ext, t4);
         } else {
-            issue_row<K, V4>(own, t4, w);
-            if (has_x) issue_row<K, V4>(ext, t4, w);
+            issue_row<K, V4, CK>(own, t4, w);
+            if (has_x) issue_row<K, V4, CK>(ext, t4, w);
         }
         cp_commit();
     }
