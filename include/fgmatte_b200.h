@@ -132,11 +132,17 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
                          int h, int iterations, double regularization, double gradient_weight, float* fg_out,
                          float* bg_out, void* stream);
 
-/* Big-level sweep kernel choice (tuning; all produce bitwise identical results):
- * 0 = automatic (per-(band, channel) warps), 1 = per-(band, channel) warps,
+/* Big-level sweep kernel choice (tuning): 0 = automatic (per-(band, channel)
+ * warps, rank-one form of the 2x2 solve), 1 = the same kernel,
  * 2 = full-channel warps (coefficients once per pixel, handed down by shuffle),
- * 3 = band CTAs: three channel warps fed by one coefficient warp (K <= 2). */
+ * 3 = band CTAs: three channel warps fed by one coefficient warp (K <= 2).
+ * Modes 2 and 3 use the adjugate form (bitwise equal to each other) and agree
+ * with mode 0/1 within the fp32 tolerance. */
 void fgm_set_sweep_mode(int mode);
+/* Tuning/debug: 1 computes the I/alpha pyramid of all sub-top levels in one
+ * pass over the full-res input (pyramid_kernel), 0 (default) with one resample
+ * launch per level (image.cpp:114-133 each).  Both are bitwise identical. */
+void fgm_set_pyramid_mode(int fused);
 
 /* Profiling: when enabled, every kernel launch of the solver is bracketed by
  * CUDA events on its stream; fgm_kernel_stats() synchronises on the recorded

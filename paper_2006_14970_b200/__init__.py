@@ -117,6 +117,7 @@ def _load():
                                        vp]
     L.fgm_profile_enable.argtypes = [C.c_int]
     L.fgm_set_sweep_mode.argtypes = [C.c_int]
+    L.fgm_set_pyramid_mode.argtypes = [C.c_int]
     L.fgm_kernel_stats.argtypes = [C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]
     L.fgm_profile_timeline.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -140,6 +141,11 @@ def device_count() -> int:
 def set_sweep_mode(mode: int) -> None:
     """0 automatic, 1 per-(band, channel) warps, 2 full-channel warps."""
     _load().fgm_set_sweep_mode(int(mode))
+
+
+def set_pyramid_mode(fused: int) -> None:
+    """1 fused I/alpha pyramid, 0 (default) one resample launch per level."""
+    _load().fgm_set_pyramid_mode(int(fused))
 
 
 def version() -> str:

@@ -18,6 +18,26 @@ struct ResampleJob {
     int idx32;                     // every src/dst element index fits in int32 (set by the host)
 };
 
+// ---- K1': the I/alpha pyramid of every big sub-top level of an image in one
+// pass over the full-resolution input (image.cpp:114-133 per level) ---------
+constexpr int kMaxPyr = 12;
+constexpr int kPyrTH = 16, kPyrTW = 128;  // full-res tile (plus one overlap row and column)
+
+struct PyrJob {
+    const float* img;    // full-res, 3 planes, dense
+    const float* alpha;
+    int W, H;
+    int nlev;
+    int tile_base;       // first tile of this job in the launch's flat tile space
+    int tcols;           // tiles per full-res tile row
+    int lw[kMaxPyr], lh[kMaxPyr], pitch[kMaxPyr];
+    double sx[kMaxPyr], sy[kMaxPyr];    // double(W)/double(lw), double(H)/double(lh) (image.cpp:73)
+    double rsx[kMaxPyr], rsy[kMaxPyr];  // their reciprocals (tile-range estimates only)
+    float* out[kMaxPyr];  // 4 pitched planes I0, I1, I2, alpha (plane stride pitch * lh)
+};
+inline int pyramid_tiles(int W, int H) { return ((W + kPyrTW - 1) / kPyrTW) * ((H + kPyrTH - 1) / kPyrTH); }
+cudaError_t launch_pyramid(const PyrJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s);
+
 // ---- K4: coarse levels, one CTA per image, shared-memory resident ---------
 constexpr int kMaxCoarseLevels = 24;
 constexpr int kCoarseCap = 2048;  // max pixels of a level handled by K4

@@ -339,8 +339,188 @@ cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long to
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int gx = int(std::min<long long>(total_tiles, (long long)sms * blocks_per_sm));
+    // blocks_per_sm 0: one tile per block (no persistent blocks holding SM slots)
+    const int gx = int(blocks_per_sm > 0 ? std::min<long long>(total_tiles, (long long)sms * blocks_per_sm) : total_tiles);
     resample_kernel<<<gx, kResCols, 0, s>>>(jobs_dev, njobs, int(total_tiles));
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------
+// K1': the I/alpha pyramid in one pass.  Every sub-top level is a bilinear
+// resize of the FULL-RESOLUTION input (multilevel.cpp:154-156 resizes the
+// original for each level), so the per-level K1 launches read the input ~2x
+// over (all rows for the ~2x level, half of them for the ~4x level, ...).
+// Here a block stages a kPyrTH x kPyrTW full-res tile (plus one overlap row
+// and column) of the four planes in shared memory once and emits, for every
+// level, the outputs whose first taps (i0) fall inside the tile: their second
+// taps (i1 = i0 + 1 or the clamped edge) are then inside the staged window.
+// Taps and arithmetic are those of resample_tile (bitwise identical output).
+constexpr int kPyrThreads = 256;
+constexpr int kPyrSW = kPyrTW + 4;           // staged row: 33 16-byte chunks (column 128 + padding)
+constexpr int kPyrPlane = (kPyrTH + 1) * kPyrSW;
+constexpr int kPyrBuf = 4 * kPyrPlane;
+
+// Smallest destination index whose first tap is >= r (dst if none): the
+// analytic estimate, then exact checks with the reference taps (i0 is
+// non-decreasing in the destination index).
+__device__ __forceinline__ int pyr_first(int r, int src, int dst, double scale, double rscale) {
+    if (r <= 0) return 0;
+    if (r > src - 1) return dst;
+    int d = int(ceil((double(r) + 0.5) * rscale - 0.5));  // (an estimate: the loops below are exact)
+    d = max(0, min(d, dst));
+    while (d > 0 && make_tap_s(d - 1, src, scale).i0 >= r) --d;
+    while (d < dst && make_tap_s(d, src, scale).i0 < r) ++d;
+    return d;
+}
+
+struct PyrTile {
+    int job, R0, C0, rows, cols;
+};
+
+// `job` advances monotonically per block (tiles are walked in increasing order)
+__device__ __forceinline__ PyrTile pyr_tile(const PyrJob* __restrict__ jobs, int njobs, int gt, int job) {
+    int lo = job;
+    while (lo + 1 < njobs && jobs[lo + 1].tile_base <= gt) ++lo;
+    const PyrJob& J = jobs[lo];
+    const int tile = gt - J.tile_base;
+    const int tyi = tile / J.tcols, txi = tile - tyi * J.tcols;
+    PyrTile t;
+    t.job = lo;
+    t.R0 = tyi * kPyrTH;
+    t.C0 = txi * kPyrTW;
+    t.rows = min(kPyrTH + 1, J.H - t.R0);
+    t.cols = min(kPyrTW + 1, J.W - t.C0);
+    return t;
+}
+
+// cp.async staging of a tile's four planes (16-byte chunks when every row of
+// the input is 16-byte aligned; the chunk past the row end is zero-filled and
+// never read), and the per-level output ranges of the tile (threads < 4 nlev).
+__device__ __forceinline__ void pyr_stage(const PyrJob& J, const PyrTile& t, unsigned sbuf, int (*rng)[4], int tid) {
+    const int W = J.W;
+    const long long HW = (long long)W * J.H;
+    const bool v4 = (W & 3) == 0 && ((reinterpret_cast<uintptr_t>(J.img) | reinterpret_cast<uintptr_t>(J.alpha)) & 15) == 0;
+    const int warp = tid >> 5, lane = tid & 31;
+    const float* img = J.img + (long long)t.R0 * W + t.C0;
+    const float* alp = J.alpha + (long long)t.R0 * W + t.C0;
+    if (v4) {
+        const int nch = (t.cols + 3) >> 2;  // <= 33 chunks per row
+        for (int r = warp; r < t.rows; r += kPyrThreads / 32) {
+            for (int c4 = lane; c4 < nch; c4 += 32) {
+                const int c = 4 * c4;
+                const int bytes = min(4, W - (t.C0 + c)) * 4;
+                const long long g = (long long)r * W + c;
+                const unsigned d = sbuf + 4u * unsigned(r * kPyrSW + c);
+                const float* src[4] = {img + g, img + HW + g, img + 2 * HW + g, alp + g};
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d + 4u * unsigned(p * kPyrPlane)),
+                                 "l"(src[p]), "r"(bytes)
+                                 : "memory");
+            }
+        }
+    } else {
+        for (int r = warp; r < t.rows; r += kPyrThreads / 32) {
+            for (int c = lane; c < t.cols; c += 32) {
+                const long long g = (long long)r * W + c;
+                const unsigned d = sbuf + 4u * unsigned(r * kPyrSW + c);
+                const float* src[4] = {img + g, img + HW + g, img + 2 * HW + g, alp + g};
+#pragma unroll
+                for (int p = 0; p < 4; ++p) cp_async_f32(d + 4u * unsigned(p * kPyrPlane), src[p]);
+            }
+        }
+    }
+    if (tid < 4 * J.nlev) {
+        const int l = tid >> 2, b = tid & 3;
+        rng[l][b] = b < 2 ? pyr_first(t.R0 + (b & 1) * kPyrTH, J.H, J.lh[l], J.sy[l], J.rsy[l])
+                          : pyr_first(t.C0 + (b & 1) * kPyrTW, W, J.lw[l], J.sx[l], J.rsx[l]);
+    }
+}
+
+// Persistent blocks, double-buffered: the next tile's loads are in flight
+// while this tile's outputs are interpolated.
+__global__ void __launch_bounds__(kPyrThreads) pyramid_kernel(const PyrJob* __restrict__ jobs, int njobs,
+                                                              int total_tiles) {
+    extern __shared__ float4 pyr_sm4[];
+    float* sm = reinterpret_cast<float*>(pyr_sm4);
+    const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sm));
+    __shared__ int rng[2][kMaxPyr][4];  // per buffer and level: first/end output row, first/end output column
+    const int tid = threadIdx.x;
+    int gt = blockIdx.x;
+    if (gt >= total_tiles) return;
+    PyrTile cur = pyr_tile(jobs, njobs, gt, 0);
+    pyr_stage(jobs[cur.job], cur, sbase, rng[0], tid);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int it = 0;; ++it) {
+        const int b = it & 1;
+        const int gn = gt + gridDim.x;
+        PyrTile nxt = cur;
+        if (gn < total_tiles) {
+            nxt = pyr_tile(jobs, njobs, gn, cur.job);
+            pyr_stage(jobs[nxt.job], nxt, sbase + 4u * unsigned((b ^ 1) * kPyrBuf), rng[b ^ 1], tid);
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;" ::: "memory");
+        __syncthreads();  // this tile's window and ranges are visible
+        {
+            // warps over output rows, lanes over output columns (coalesced
+            // stores, no index division); a lane's x-taps are computed once per
+            // level and reused for every row
+            const PyrJob& J = jobs[cur.job];
+            const int W = J.W, H = J.H, nlev = J.nlev;
+            const int warp = tid >> 5, lane = tid & 31;
+            const float* buf = sm + b * kPyrBuf;
+            for (int l = 0; l < nlev; ++l) {
+                const int dy0 = rng[b][l][0], ny = rng[b][l][1] - dy0, dx0 = rng[b][l][2], nx = rng[b][l][3] - dx0;
+                if (ny <= 0 || nx <= 0) continue;
+                const int pitch = J.pitch[l];
+                const long long ps = (long long)pitch * J.lh[l];
+                float* out = J.out[l] + (long long)dy0 * pitch + dx0;
+                const double sx = J.sx[l], sy = J.sy[l];
+                for (int x0 = 0; x0 < nx; x0 += 32) {
+                    const int xi = x0 + lane;
+                    if (xi >= nx) break;
+                    const Tap tx = make_tap_s(dx0 + xi, W, sx);
+                    const int cx = tx.i0 - cur.C0, dx = tx.i1 - tx.i0;
+                    for (int yi = warp; yi < ny; yi += kPyrThreads / 32) {
+                        const Tap ty = make_tap_s(dy0 + yi, H, sy);
+                        const int a0 = (ty.i0 - cur.R0) * kPyrSW + cx;
+                        const int c0 = (ty.i1 - cur.R0) * kPyrSW + cx;
+                        float* d = out + (long long)yi * pitch + xi;
+                        float v[4];
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) {
+                            const float* s = buf + p * kPyrPlane;
+                            v[p] = bilerp(s[a0], s[a0 + dx], s[c0], s[c0 + dx], tx.t, ty.t);
+                        }
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) d[p * ps] = v[p];
+                    }
+                }
+            }
+        }
+        __syncthreads();  // buffer b (and its ranges) are free for the tile after next
+        if (gn >= total_tiles) break;
+        gt = gn;
+        cur = nxt;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+cudaError_t launch_pyramid(const PyrJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s) {
+    if (njobs <= 0 || total_tiles <= 0) return cudaSuccess;
+    constexpr size_t smem = size_t(2) * kPyrBuf * sizeof(float);
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        cudaError_t e = cudaFuncSetAttribute(pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pyramid_kernel, kPyrThreads, smem);
+        per_sm = std::max(per_sm, 1);
+    }
+    const int gx = int(std::min<long long>(total_tiles, (long long)sms * per_sm));
+    pyramid_kernel<<<gx, kPyrThreads, smem, s>>>(jobs_dev, njobs, int(total_tiles));
     return cudaGetLastError();
 }
 

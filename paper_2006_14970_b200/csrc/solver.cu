@@ -407,6 +407,12 @@ std::vector<int2> band_order(const std::vector<SweepJob>& sj, bool full) {
 // 1 full-channel warps (sweep_full.cu), 2 band CTAs with a shared
 // coefficient warp (sweep_cta.cu).  All three are bitwise identical.
 int g_sweep_mode = 0;  // 0 auto, 1 per-channel, 2 full-channel, 3 band CTA
+// 1: fused I/alpha pyramid (pyramid_kernel), 0: one resample launch per level
+// (FGM_PYRAMID in the environment sets the initial value)
+int g_pyramid_mode = [] {  // default per level: the fused pass measured slower
+    const char* e = std::getenv("FGM_PYRAMID");
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : 0;
+}();
 int sweep_kind(int total_bands, int K) {
     (void)total_bands;
     if (g_sweep_mode == 2 && K <= 3) return 1;  // the full-channel kernel's state does not fit beyond K = 3
@@ -425,7 +431,7 @@ cudaError_t launch_sweep_kind(int kind, int K, const SweepJob* jd, const int2* o
     }
 }
 
-enum LaunchKind { kCoarse, kResample, kUpsample, kSweep, kCopy };
+enum LaunchKind { kCoarse, kResample, kUpsample, kSweep, kCopy, kPyramid };
 struct LaunchRec {
     LaunchKind kind;
     int K, njobs, total_bands;
@@ -444,8 +450,21 @@ struct LaunchRec {
 // upsamples and sweeps), and a pool of events.
 struct SideStream {
     int dev = -1;
+    int prio_hi = 0;
     cudaStream_t s = nullptr;
     std::vector<cudaEvent_t> ev;
+    // high-priority twins of the caller's streams: the main work of a solve
+    // runs there, so the scheduler hands freed SM slots to its blocks before
+    // the pyramid's (a caller stream has the default, lowest, priority)
+    std::vector<std::pair<cudaStream_t, cudaStream_t>> hi;
+    cudaStream_t high(cudaStream_t caller) {
+        for (auto& h : hi)
+            if (h.first == caller) return h.second;
+        cudaStream_t t;
+        ck(cudaStreamCreateWithPriority(&t, cudaStreamNonBlocking, prio_hi), "cudaStreamCreate");
+        hi.emplace_back(caller, t);
+        return t;
+    }
     cudaEvent_t event(size_t i) {
         while (ev.size() <= i) {
             cudaEvent_t e;
@@ -459,7 +478,13 @@ thread_local SideStream g_side;
 #ifndef FGM_SIDE_BLOCKS
 #define FGM_SIDE_BLOCKS 16
 #endif
-constexpr int kSideBlocksPerSM = FGM_SIDE_BLOCKS;
+int side_blocks_per_sm() {  // (tuning knob FGM_SIDE_BLOCKS_RT overrides; 0 = one tile per block)
+    static const int v = [] {
+        const char* e = std::getenv("FGM_SIDE_BLOCKS_RT");
+        return e ? std::atoi(e) : FGM_SIDE_BLOCKS;
+    }();
+    return v;
+}
 
 SideStream& side_stream() {
     int dev = 0;
@@ -468,7 +493,10 @@ SideStream& side_stream() {
         g_side = SideStream{};
         int lo = 0, hi = 0;  // lowest priority: its blocks yield SM slots to the main stream's
         ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
-        ck(cudaStreamCreateWithPriority(&g_side.s, cudaStreamNonBlocking, lo), "cudaStreamCreate");
+        const char* e = std::getenv("FGM_SIDE_HI");  // (tuning knob: pyramid at the highest priority)
+        ck(cudaStreamCreateWithPriority(&g_side.s, cudaStreamNonBlocking, e && std::atoi(e) ? hi : lo),
+           "cudaStreamCreate");
+        g_side.prio_hi = hi;
         g_side.dev = dev;
     }
     return g_side;
@@ -537,8 +565,55 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
     }
 
     // ---- I/alpha pyramid of every big sub-top level, on the side stream ----
-    // (step j's launch records event j; step j's sweep waits for it)
-    for (int j = 0; j < J; ++j) {
+    // Fused (default): one pass over each full-res input emits every level
+    // (pyramid_kernel); its event (index J + 3) gates the first sweep of
+    // every sub-top level.  Per level (FGM_PYRAMID=0): step j's resample
+    // launch records event j and step j's sweep waits for it.
+    const bool fused_pyr = g_pyramid_mode != 0;
+    bool pyr_fits = true;
+    for (const auto& P : plans) pyr_fits = pyr_fits && int(P.lv.size()) - 1 - P.nc <= kMaxPyr;
+    const int pyr_ev = J + 3;
+    bool pyr_launch = false;
+    if (fused_pyr && pyr_fits) {
+        std::vector<PyrJob> pj;
+        long long tiles = 0;
+        double bytes = 0;
+        for (auto& P : plans) {
+            const int n = int(P.lv.size());
+            PyrJob q{};
+            q.img = P.io.img;
+            q.alpha = P.io.alpha;
+            q.W = P.io.W;
+            q.H = P.io.H;
+            for (int l = P.nc; l < n - 1; ++l) {
+                const Level L = P.lv[size_t(l)];
+                q.lw[q.nlev] = L.w;
+                q.lh[q.nlev] = L.h;
+                q.pitch[q.nlev] = level_pitch(L.w);
+                q.sx[q.nlev] = double(P.io.W) / double(L.w);  // make_taps' scale, image.cpp:73
+                q.sy[q.nlev] = double(P.io.H) / double(L.h);
+                q.rsx[q.nlev] = 1.0 / q.sx[q.nlev];
+                q.rsy[q.nlev] = 1.0 / q.sy[q.nlev];
+                q.out[q.nlev] = P.lvlIA + P.ia_off[size_t(l)];
+                bytes += 16.0 * double(L.w) * L.h;
+                ++q.nlev;
+            }
+            if (q.nlev == 0) continue;
+            q.tcols = (q.W + kPyrTW - 1) / kPyrTW;
+            q.tile_base = int(tiles);
+            tiles += pyramid_tiles(q.W, q.H);
+            bytes += 16.0 * double(q.W) * q.H * (1.0 + 1.0 / kPyrTH);
+            pj.push_back(q);
+        }
+        if (!pj.empty()) {
+            LaunchRec lr{kPyramid, 0, int(pj.size()), 0, false, st.push(pj), 0, 0, tiles, bytes};
+            lr.side = 1;
+            lr.ev = pyr_ev;
+            launches.push_back(lr);
+            pyr_launch = true;
+        }
+    }
+    for (int j = 0; j < J && !pyr_launch; ++j) {
         std::vector<ResampleJob> rj;
         long long tiles = 0;
         double rbytes = 0;
@@ -567,7 +642,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
     }
     std::vector<char> has_ia(size_t(J), 0);
     for (const auto& r : launches)
-        if (r.side) has_ia[size_t(r.ev)] = 1;
+        if (r.side && r.kind == kResample) has_ia[size_t(r.ev)] = 1;
 
     // ---- big levels, aligned so that every image's top level is step J-1 --
     for (int j = 0; j < J; ++j) {
@@ -676,6 +751,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 const size_t ooff = st.push(band_order(sj, per_band(sk)));
                 LaunchRec lr{kSweep, K, int(sj.size()), total, sk, off, ticket, ooff, (long long)max_stream, sbytes};
                 if (pi == 0 && has_ia[size_t(j)]) lr.ev = j;  // this step's I/alpha pyramid level
+                if (pi == 0 && pyr_launch && j < J - 1) lr.ev = pyr_ev;
                 launches.push_back(lr);
             }
         }
@@ -706,25 +782,63 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
     // job uploads) and s waits for all of its work at the end
     SideStream& side = side_stream();
     const cudaEvent_t ev_start = side.event(size_t(J)), ev_end = side.event(size_t(J) + 1);
+    // (tuning knob FGM_PYRAMID_MAIN=1: the I/alpha pyramid runs first, on the
+    // main stream, instead of overlapping the coarse and small levels)
+    static const bool pyr_main = [] {
+        const char* e = std::getenv("FGM_PYRAMID_MAIN");
+        return e && std::atoi(e) != 0;
+    }();
     bool any_side = false;
     for (const LaunchRec& r : launches) any_side = any_side || r.side;
+    any_side = any_side && !pyr_main;
+    // tuning knob FGM_MAIN_HI=1: main work on the caller stream's high-priority twin
+    static const bool main_hi = [] {  // (default off: measured neutral on the C4 batch)
+        const char* e = std::getenv("FGM_MAIN_HI");
+        return e && std::atoi(e) != 0;
+    }();
+    const cudaStream_t caller = s;
     if (any_side) {
         ck(cudaEventRecord(ev_start, s), "cudaEventRecord");
         ck(cudaStreamWaitEvent(side.s, ev_start, 0), "cudaStreamWaitEvent");
+        if (main_hi) {
+            s = side.high(caller);
+            ck(cudaStreamWaitEvent(s, ev_start, 0), "cudaStreamWaitEvent");
+        }
     }
 
+    if (pyr_main) {
+        for (const LaunchRec& r : launches) {
+            if (!r.side) continue;
+            ProfScope ps(s, 1, r.bytes);
+            if (r.kind == kPyramid)
+                ck(launch_pyramid(reinterpret_cast<const PyrJob*>(djobs + r.job_off), r.njobs, r.max_rows, s),
+                   "pyramid_kernel");
+            else
+                ck(launch_resample(reinterpret_cast<const ResampleJob*>(djobs + r.job_off), r.njobs, r.max_rows, s),
+                   "resample_kernel");
+        }
+    }
     for (const LaunchRec& r0 : launches) {
         const LaunchRec& r = r0;
+        if (r.side && pyr_main) continue;
+        if (r.side && r.kind == kPyramid) {  // the whole I/alpha pyramid
+            ProfScope ps(side.s, 1, r.bytes);
+            ck(launch_pyramid(reinterpret_cast<const PyrJob*>(djobs + r.job_off), r.njobs, r.max_rows, side.s),
+               "pyramid_kernel");
+            ck(cudaEventRecord(side.event(size_t(r.ev)), side.s), "cudaEventRecord");
+            continue;
+        }
         if (r.side) {  // I/alpha pyramid level
             ProfScope ps(side.s, 1, r.bytes);
             ck(launch_resample(reinterpret_cast<const ResampleJob*>(djobs + r.job_off), r.njobs, r.max_rows, side.s,
-                               kSideBlocksPerSM),
+                               side_blocks_per_sm()),
                "resample_kernel");
             ck(cudaEventRecord(side.event(size_t(r.ev)), side.s), "cudaEventRecord");
             continue;
         }
-        if (r.ev >= 0) ck(cudaStreamWaitEvent(s, side.event(size_t(r.ev)), 0), "cudaStreamWaitEvent");
+        if (r.ev >= 0 && !pyr_main) ck(cudaStreamWaitEvent(s, side.event(size_t(r.ev)), 0), "cudaStreamWaitEvent");
         switch (r.kind) {
+            case kPyramid: break;  // (side stream only)
             case kCoarse: {
                 ProfScope ps(s, 2, r.bytes);
                 ck(launch_coarse(reinterpret_cast<const CoarseJob*>(djobs + r.job_off), r.njobs, eps, omega, s),
@@ -766,7 +880,13 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
     }
     if (any_side) {  // nothing of this call stays outstanding on the side stream
         ck(cudaEventRecord(ev_end, side.s), "cudaEventRecord");
-        ck(cudaStreamWaitEvent(s, ev_end, 0), "cudaStreamWaitEvent");
+        ck(cudaStreamWaitEvent(caller, ev_end, 0), "cudaStreamWaitEvent");
+        if (s != caller) {  // nor on the high-priority twin
+            const cudaEvent_t ev_main = side.event(size_t(J) + 2);
+            ck(cudaEventRecord(ev_main, s), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(caller, ev_main, 0), "cudaStreamWaitEvent");
+        }
+        s = caller;
     }
 }
 
@@ -1179,6 +1299,7 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
 }
 
 void fgm_set_sweep_mode(int mode) { g_sweep_mode = (mode >= 0 && mode <= 3) ? mode : 0; }
+void fgm_set_pyramid_mode(int fused) { g_pyramid_mode = fused ? 1 : 0; }
 
 void fgm_profile_enable(int on) {
     std::lock_guard<std::mutex> g(g_prof_mu);

@@ -374,6 +374,35 @@ def test_batch_equals_single_bitwise(fgm, cuda):
         assert torch.equal(f, f1) and torch.equal(b, b1)
 
 
+def test_fused_pyramid_bitwise(fgm, cuda):
+    # one pass over the full-res input for every level's I/alpha (pyramid_kernel)
+    # == one resample launch per level (image.cpp:114-133): same taps, same
+    # arithmetic, so identical levels and identical solves; sizes cover ragged
+    # tiles, 1-pixel-wide/-high images and a level with an unchanged height
+    from paper_2006_14970_b200 import synth
+
+    sizes = [(300, 200), (513, 257), (1000, 33), (2, 700), (700, 3), (129, 17), (777, 1)]
+    imgs, alps = [], []
+    for i, (w, h) in enumerate(sizes):
+        im, al = synth.make_composite(w, h, 950 + i, 3, 3.0)
+        imgs.append(im.to(cuda))
+        alps.append(al.to(cuda))
+    try:
+        fgm.set_pyramid_mode(0)
+        a = fgm.batch_solve_cuda(imgs, alps, fgm.BASELINE_PARAMS)
+        la = [fgm.ml_foreground_background_levels_cuda(im, al, fgm.BASELINE_PARAMS) for im, al in zip(imgs, alps)]
+        fgm.set_pyramid_mode(1)
+        b = fgm.batch_solve_cuda(imgs, alps, fgm.BASELINE_PARAMS)
+        lb = [fgm.ml_foreground_background_levels_cuda(im, al, fgm.BASELINE_PARAMS) for im, al in zip(imgs, alps)]
+    finally:
+        fgm.set_pyramid_mode(0)
+    for (fa, ba), (fb, bb) in zip(a, b):
+        assert torch.equal(fa, fb) and torch.equal(ba, bb)
+    for x, y in zip(la, lb):
+        for lx, ly in zip(x[2] + x[3], y[2] + y[3]):
+            assert torch.equal(lx, ly)
+
+
 @pytest.mark.parametrize("kw", [dict(), dict(iters_high=1), dict(iters_high=3), dict(iters_high=5)])
 def test_sweep_kernels_agree_bitwise(fgm, cuda, oracle_mod, kw):
     # the two experimental K3 variants (full-channel warps with passed
