@@ -371,8 +371,46 @@ struct StepCtx {
 // border occurs (x <= 0): the L clamp and the bounds of the stream and the
 // flush, as selects and predicates.  Every band's start is on the chain's
 // critical path (the band below waits for it).
+// Per-group addressing of the interior paths.  With K = 2 (mod 4) a group's
+// four flushed output rows never cross a 16-row half of the output ring
+// (u = t - (K-1) - 15 starts the group at a multiple of 4), so step s of the
+// group flushes row jf0 + s of segment xs0: the global addresses advance by
+// one output row per step and the ring offsets by one ring row, and lane 31's
+// boundary-stream slot by 2K floats (an immediate offset).
+template <int K>
+struct GroupAddr {
+    float* fo;        // flush address of step 0, F plane
+    float* bo;        // and B plane
+    int o0;           // output-ring float index of step 0
+    bool seg_ok;      // XL: the segment start column is inside the row
+    int jf0;          // flushed band row of step 0
+    float* sdst;      // lane 31's boundary-stream slot of step 0
+};
+template <int K>
+__device__ __forceinline__ constexpr bool group_addr_ok() { return K % 4 == 2; }
+
+template <int K, int CK>
+__device__ __forceinline__ GroupAddr<K> group_addr(const StepCtx<K>& x_, int t4) {
+    using Gm = Geom<K, CK>;
+    constexpr int OW = Gm::OW;
+    GroupAddr<K> g;
+    const int lane = x_.lane;
+    const int col = lane & (OW - 1);
+    const int u0 = t4 - (K - 1) - (OW - 1);
+    g.jf0 = (u0 & (OW - 1)) + (lane & 16);
+    const int xs0 = (u0 & ~(OW - 1)) - (lane & 16);
+    g.seg_ok = xs0 >= 0;
+    const unsigned off = unsigned(g.jf0 * x_.opitch + xs0 + col);  // (used only when seg_ok)
+    g.fo = x_.FO + off;
+    g.bo = x_.BO + off;
+    g.o0 = Gm::OFF_O + orow(g.jf0) * OW + col;
+    g.sdst = x_.my_stream + (long long)(t4 - 31) * K * 2;
+    return g;
+}
+
 template <int K, bool G, int CK, bool Y = false, bool XL = false>
-__device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_, int tr) {
+__device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_, int tr,
+                                          const GroupAddr<K>* ga = nullptr, int gs = 0) {
     using Gm = Geom<K, CK>;
     constexpr int OW = Gm::OW;
     const int lane = x_.lane, y0 = x_.y0, w = x_.w, h = x_.h;
@@ -443,7 +481,7 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
 
     // boundary stream for the band below: lane 31's K outputs of this step
     if (x_.has_down && lane == kBandRows - 1 && (!(G || XL) || (tr - 31 >= 0 && tr - 31 < x_.Umax))) {
-        float* dst = x_.my_stream + size_t(tr - 31) * K * 2;
+        float* dst = (!G && group_addr_ok<K>() && ga) ? ga->sdst + gs * K * 2 : x_.my_stream + size_t(tr - 31) * K * 2;
         if (K % 2 == 0) {  // 16-byte aligned: u * 2K floats with K even
 #pragma unroll
             for (int k = 0; k + 1 < K; k += 2)
@@ -458,7 +496,20 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
     // flush completed 16-column output row segments: rows jf (lanes 0-15) and
     // jf+16 (lanes 16-31), one coalesced 64-byte store per plane each.
     // Offsets are 32-bit, relative to the band's first output row.
-    {
+    if (!G && group_addr_ok<K>() && ga) {
+        bool ok = true;
+        if (Y) {
+            const int yf = y0 + ga->jf0 + gs - (K - 1);
+            ok = yf >= 0 && yf < h;
+        }
+        if (XL) ok = ok && ga->seg_ok;
+        if (ok) {
+            const long long ro = (long long)gs * x_.opitch;
+            const int o = ga->o0 + gs * OW;
+            stg(ga->fo + ro, lds(o));
+            stg(ga->bo + ro, lds(o + Gm::OPL));
+        }
+    } else {
         const int col = lane & (OW - 1);
         const int u = tr - (K - 1) - (OW - 1);
         const int jf = (u & (OW - 1)) + (lane & 16);
@@ -636,18 +687,22 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
             }
             __syncwarp();
             if (t4 >= fast_lo && t4 + S <= fast_hi && !yband) {
+                const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
 #pragma unroll
-                for (int s = 0; s < S; ++s) band_step<K, false, CK>(st, cx, t4 + s);
+                for (int s = 0; s < S; ++s) band_step<K, false, CK>(st, cx, t4 + s, &ga, s);
             } else if (t4 >= fast_lo && t4 + S <= fast_hi) {
+                const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
 #pragma unroll
-                for (int s = 0; s < S; ++s) band_step<K, false, CK, true>(st, cx, t4 + s);
+                for (int s = 0; s < S; ++s) band_step<K, false, CK, true>(st, cx, t4 + s, &ga, s);
             } else if (t4 < fast_lo && t4 + S <= fast_hi) {  // band start: left border only
                 if (yband) {
+                    const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
 #pragma unroll
-                    for (int s = 0; s < S; ++s) band_step<K, false, CK, true, true>(st, cx, t4 + s);
+                    for (int s = 0; s < S; ++s) band_step<K, false, CK, true, true>(st, cx, t4 + s, &ga, s);
                 } else {
+                    const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
 #pragma unroll
-                    for (int s = 0; s < S; ++s) band_step<K, false, CK, false, true>(st, cx, t4 + s);
+                    for (int s = 0; s < S; ++s) band_step<K, false, CK, false, true>(st, cx, t4 + s, &ga, s);
                 }
             } else {
 #pragma unroll 1
