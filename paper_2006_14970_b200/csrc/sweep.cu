@@ -253,6 +253,79 @@ __device__ __forceinline__ void issue_row_fast(const RowSrc& rs, int t4) {
     }
 }
 
+// Interior groups of interior bands, flattened: the 130 + 2K (plane, band
+// row) blocks a group issues (alpha rows -K..32, image rows -(K-1)..31, F and
+// B rows 0..32) are dealt to the lanes of ceil((130 + 2K) / 32) cp.async
+// instructions instead of one own-row and one extra-row instruction per plane
+// (the extra rows occupy three lanes).  Per lane and instruction: the row's
+// global base, its ring address and its lead q = S + L - r, all fixed per band.
+template <int K>
+struct FlatSrc {
+    static constexpr int N = (130 + 2 * K + 31) / 32;
+    const float* g[N];
+    unsigned s[N];
+    int q[N];
+    unsigned on;  // bit i: lane holds an item in instruction i
+};
+
+template <int K, int CK>
+__device__ __forceinline__ FlatSrc<K> make_flat(const SweepJob& J, int ch, int y0, int lane, unsigned sbase) {
+    using G = Geom<K, CK>;
+    FlatSrc<K> f;
+    f.on = 0;
+    constexpr int NAl = 33 + K, NIm = 31 + K, NFB = 33;
+#pragma unroll
+    for (int i = 0; i < FlatSrc<K>::N; ++i) {
+        int it = 32 * i + lane;
+        int p = 0, r = 0;
+        if (it < NAl) {
+            p = 0;
+            r = it - K;
+        } else if ((it -= NAl) < NIm) {
+            p = 1;
+            r = it - (K - 1);
+        } else if ((it -= NIm) < NFB) {
+            p = 2;
+            r = it;
+        } else if ((it -= NFB) < NFB) {
+            p = 3;
+            r = it;
+        } else {
+            p = -1;
+        }
+        const int y = min(max(y0 + r, 0), J.h - 1);  // (in range for interior bands)
+        const float* base = p == 0 ? J.alpha + (long long)y * J.ipitch
+                          : p == 1 ? J.img + ch * J.istride + (long long)y * J.ipitch
+                          : p == 2 ? J.fg_in + ch * J.fstride + (long long)y * J.fpitch
+                                   : J.bg_in + ch * J.fstride + (long long)y * J.fpitch;
+        f.g[i] = base;
+        const int po = p == 0 ? plane_off<K>(0) : p == 1 ? plane_off<K>(1) : p == 2 ? plane_off<K>(2) : plane_off<K>(3);
+        f.s[i] = sbase + 4u * unsigned(po + r * G::RS);
+        f.q[i] = G::S + G::L - r;
+        if (p >= 0) f.on |= 1u << i;
+    }
+    return f;
+}
+
+template <int K, int CK>
+__device__ __forceinline__ void issue_flat(const FlatSrc<K>& f, int t4) {
+    using G = Geom<K, CK>;
+#pragma unroll
+    for (int i = 0; i < FlatSrc<K>::N; ++i) {
+        const unsigned x0 = unsigned(t4 + f.q[i]) & ~unsigned(G::S - 1);
+        const unsigned c = x0 & (G::RW - 1);
+        const float* g = f.g[i] + x0;
+        const unsigned d = f.s[i] + 4u * c;
+        const unsigned on = (f.on >> i) & 1u;
+#pragma unroll
+        for (int b = 0; b < G::S / 4; ++b) {
+            cp_async16_if(d + 16u * b, g + 4 * b, on);
+            if (4 * b < G::MIR)
+                cp_async16_if(d + 16u * b + 4u * G::RW, g + 4 * b, on & (c + 4u * b < unsigned(G::MIR) ? 1u : 0u));
+        }
+    }
+}
+
 // Everything issued "before group t0".
 template <int K, bool V4, int CK>
 __device__ __forceinline__ void prologue_row(const RowSrc& rs, int t0, int w) {
@@ -631,6 +704,12 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     const bool has_x = lane >= 32 - K || lane == 0;
     const RowSrc ext =
         make_rowsrc<K>(J, ch, y0, lane == 0 ? 32 : lane - 32, has_x, lane >= 33 - K, lane == 0, sbase);
+#ifndef FGM_FLAT_ISSUE
+#define FGM_FLAT_ISSUE 1
+#endif
+#if FGM_FLAT_ISSUE
+    const FlatSrc<K> flat = make_flat<K, CK>(J, ch, y0, lane, sbase);
+#endif
 
     LaneState<K> st;
 #pragma unroll
@@ -711,8 +790,12 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
         }
         __syncwarp();  // every lane is done with the ring slots the next loads overwrite
         if (V4 && !yband && t4 >= issue_lo && t4 < issue_hi) {
+#if FGM_FLAT_ISSUE
+            issue_flat<K, CK>(flat, t4);
+#else
             issue_row_fast<K, 15u, CK>(own, t4);
             issue_row_fast<K, 0u, CK>(ext, t4);
+#endif
         } else {
             issue_row<K, V4, CK>(own, t4, w);
             if (has_x) issue_row<K, V4, CK>(ext, t4, w);
