@@ -330,8 +330,10 @@ __device__ __forceinline__ float2 pixel_applyr(const CoefR& co, float2 L, float2
     const f32x2 m = mul2(pk2(co.iS, co.iS), s);  // (Fbar, Bbar)
     const float2 t = upk2(mul2(co.u, m));  // (u0 Fbar, u1 Bbar)
     const float r = __fsub_rn(co.I, __fadd_rn(t.x, t.y));
-    const float2 o = upk2(fma2(co.pq, pk2(r, r), m));
-    return make_float2(__saturatef(o.x), __saturatef(o.y));
+    // the update as two scalar FFMA.SAT (the same IEEE fma per half as an
+    // FFMA2, with the clamp folded in)
+    const float2 pq = upk2(co.pq), mv = upk2(m);
+    return make_float2(__saturatef(__fmaf_rn(pq.x, r, mv.x)), __saturatef(__fmaf_rn(pq.y, r, mv.y)));
 }
 
 // Neighbour-dependent part.  Values from this lane's previous step (L, D)
