@@ -613,6 +613,14 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             pyr_launch = true;
         }
     }
+    // (tuning knob FGM_PYR_LAST_MAIN=1: the largest level's I/alpha runs on the
+    // main stream right before that level instead of beside the small levels)
+    static const bool pyr_last_main = [] {
+        const char* e = std::getenv("FGM_PYR_LAST_MAIN");
+        return e && std::atoi(e) != 0;
+    }();
+    LaunchRec last_pyr{};
+    bool has_last_pyr = false;
     for (int j = 0; j < J && !pyr_launch; ++j) {
         std::vector<ResampleJob> rj;
         long long tiles = 0;
@@ -636,6 +644,11 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             tiles += resample_tiles(r.dw, r.dh);
         }
         LaunchRec lr{kResample, 0, int(rj.size()), 0, false, st.push(rj), 0, 0, tiles, rbytes};
+        if (pyr_last_main && j == J - 2) {  // runs on the main stream just before its level
+            last_pyr = lr;
+            has_last_pyr = true;
+            continue;
+        }
         lr.side = 1;
         lr.ev = j;
         launches.push_back(lr);
@@ -646,6 +659,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
 
     // ---- big levels, aligned so that every image's top level is step J-1 --
     for (int j = 0; j < J; ++j) {
+        if (has_last_pyr && j == J - 2) launches.push_back(last_pyr);
         std::vector<ResampleJob> rj, uj;  // resample (I/alpha) and upsample (F/B) jobs
         long long max_rows = 0;
         double rbytes = 0, ubytes = 0;

@@ -665,6 +665,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+#ifndef FGM_REPOLL
+#define FGM_REPOLL 1
+#endif
 template <int K, bool V4, int CK>
 __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int lane, unsigned sbase, float eps,
                                          float omega) {
@@ -757,7 +760,7 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
                     pend_ok = false;
                     if (nxt < Umax && lane_ch)  // prefetch the next chunk
                         pend = ld_relaxed_v4(up_stream + size_t(nxt) * K * 2 + 4 * lane);
-                } else if (!pend_ok && nxt < Umax) {
+                } else if (FGM_REPOLL && !pend_ok && nxt < Umax) {
                     // the prefetch found the next chunk incomplete: re-poll it
                     // now rather than a full round trip when it is needed
                     pend_ok = __all_sync(kFull, chunk_complete<K, CK>(pend, nxt, Umax, lane));
