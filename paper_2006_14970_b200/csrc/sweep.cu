@@ -813,10 +813,10 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
 }
 
 #ifndef FGM_SWEEP_MINB
-#define FGM_SWEEP_MINB 1
+#define FGM_SWEEP_MINB 1  // (12 caps the K = 2 throughput kernel at 168 registers: 9 warps per SM instead of 8; measured no faster)
 #endif
 template <int K, bool V4, int CK>
-__global__ void __launch_bounds__(32, FGM_SWEEP_MINB) sweep_kernel(const SweepJob* __restrict__ jobs, const int2* __restrict__ order,
+__global__ void __launch_bounds__(32, (K == 2 && CK >= 16) ? FGM_SWEEP_MINB : 1) sweep_kernel(const SweepJob* __restrict__ jobs, const int2* __restrict__ order,
                                                     int total_items, unsigned* ticket, float eps, float omega) {
     const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sweep_sm4));
     const int lane = threadIdx.x & 31;
@@ -848,6 +848,9 @@ cudaError_t launch_sweep_kc(const SweepJob* jobs_dev, const int2* order_dev, int
         cudaError_t e =
             cudaFuncSetAttribute(sweep_kernel<K, true, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
+        // the largest shared-memory carveout: the rings, not L1, bound the resident warps
+        e = cudaFuncSetAttribute(sweep_kernel<K, true, CK>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
         attr = true;
     }
     const int grid = std::max(1, std::min(total_items, grid_cap));
@@ -863,6 +866,8 @@ cudaError_t launch_sweep_k(const SweepJob* jobs_dev, const int2* order_dev, int 
         constexpr size_t smem = size_t(Geom<K, kChunk>::TOTAL) * sizeof(float);
         cudaError_t e = cudaFuncSetAttribute(sweep_kernel<K, true, kChunk>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(sweep_kernel<K, true, kChunk>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
