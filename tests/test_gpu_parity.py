@@ -485,3 +485,38 @@ def test_concurrent_host_threads(fgm, cuda):
     assert not errs, errs
     for (wf, wb), (gf, gb) in zip(want, got):
         assert torch.equal(wf, gf) and torch.equal(wb, gb)
+
+
+@pytest.mark.parametrize("iters_high", [2, 3, 8])
+def test_no_writes_outside_outputs(fgm, cuda, oracle_mod, iters_high):
+    # every output plane is written inside [fg, fg + 3wh) and nothing else:
+    # the outputs are views into guarded buffers whose canaries must survive
+    # (sizes: ragged bands and segments, 1-wide, 1-high, a vec4-misaligned
+    # offset), and the inputs are left untouched
+    from paper_2006_14970_b200 import synth
+
+    G = 4099  # guard floats on each side (odd: misaligns every output by 4 bytes mod 16)
+    canary = -12345.0
+    sizes = [(1, 1), (7, 3), (33, 65), (257, 129), (1000, 33), (2, 700), (700, 2), (3000, 70)]
+    imgs, alps, outs, bigs = [], [], [], []
+    for i, (w, h) in enumerate(sizes):
+        im, al = synth.make_composite(w, h, 1200 + i, 3, 3.0)
+        imgs.append(im.to(cuda))
+        alps.append(al.to(cuda))
+        n = 3 * w * h
+        pair = []
+        for _ in range(2):
+            big = torch.full((n + 2 * G,), canary, device=cuda)
+            bigs.append(big)
+            pair.append(big[G:G + n].view(3, h, w))
+        outs.append(tuple(pair))
+    before = [x.clone() for x in imgs + alps]
+    p = params_from(fgm, oracle_mod.Params(iters_high=iters_high))
+    fgm.batch_solve_cuda(imgs, alps, p, outputs=outs)
+    torch.cuda.synchronize()
+    for big in bigs:
+        assert bool((big[:G] == canary).all()) and bool((big[-G:] == canary).all())
+    for (f, b) in outs:
+        assert bool(((f >= 0) & (f <= 1)).all()) and bool(((b >= 0) & (b <= 1)).all())
+    for x, y in zip(before, imgs + alps):
+        assert torch.equal(x, y)
