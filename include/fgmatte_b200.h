@@ -144,6 +144,11 @@ void fgm_set_sweep_mode(int mode);
  * launch per level (image.cpp:114-133 each).  Both are bitwise identical. */
 void fgm_set_pyramid_mode(int fused);
 
+/* Debug: 1 surrounds every workspace region of a solve with a guard band and
+ * checks it (synchronously) when the solve's work is done; an overrun fails
+ * the call with FGM_RUNTIME_ERROR.  0 (default) off. */
+void fgm_set_debug_guards(int on);
+
 /* Profiling: when enabled, every kernel launch of the solver is bracketed by
  * CUDA events on its stream; fgm_kernel_stats() synchronises on the recorded
  * events and reports, for kernel class `which` (0 = big-level sweep K3,

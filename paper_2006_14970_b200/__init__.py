@@ -118,6 +118,7 @@ def _load():
     L.fgm_profile_enable.argtypes = [C.c_int]
     L.fgm_set_sweep_mode.argtypes = [C.c_int]
     L.fgm_set_pyramid_mode.argtypes = [C.c_int]
+    L.fgm_set_debug_guards.argtypes = [C.c_int]
     L.fgm_kernel_stats.argtypes = [C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]
     L.fgm_profile_timeline.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -146,6 +147,11 @@ def set_sweep_mode(mode: int) -> None:
 def set_pyramid_mode(fused: int) -> None:
     """1 fused I/alpha pyramid, 0 (default) one resample launch per level."""
     _load().fgm_set_pyramid_mode(int(fused))
+
+
+def set_debug_guards(on: int) -> None:
+    """1: guard bands around every workspace region, checked after each solve."""
+    _load().fgm_set_debug_guards(int(on))
 
 
 def version() -> str:

@@ -221,22 +221,48 @@ int vec4_ok(const SweepJob& j) {
 }
 
 // ---- stream-ordered workspace ----------------------------------------------
+// Debug guard mode (fgm_set_debug_guards): every carved region is followed by
+// a guard of kGuardBytes filled with a byte pattern; check_guards() (called at
+// the end of a solve, synchronously) fails the call if a kernel wrote past a
+// region (level buffers, pass ping-pong, boundary streams, job descriptors).
+int g_debug_guards = 0;
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+
 struct Arena {
     char* base = nullptr;
     size_t size = 0, off = 0;
     cudaStream_t s = nullptr;
-    void reserve(size_t bytes, cudaStream_t st) {
+    std::vector<char*> guards;
+    void reserve(size_t bytes, cudaStream_t st, size_t max_takes = 8) {
         s = st;
-        size = bytes;
-        if (bytes) ck(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, s), "cudaMallocAsync");
+        size = bytes + (g_debug_guards ? max_takes * kGuardBytes : 0);
+        if (size) ck(cudaMallocAsync(reinterpret_cast<void**>(&base), size, s), "cudaMallocAsync");
     }
     template <class T>
     T* take(size_t count) {
         const size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
-        if (off + bytes > size) throw RuntimeError("internal: arena overflow");
+        const size_t gb = g_debug_guards ? kGuardBytes : 0;
+        if (off + bytes + gb > size) throw RuntimeError("internal: arena overflow");
         T* p = reinterpret_cast<T*>(base + off);
         off += bytes;
+        if (gb) {
+            guards.push_back(base + off);
+            ck(cudaMemsetAsync(base + off, kGuardByte, gb, s), "cudaMemsetAsync(guard)");
+            off += gb;
+        }
         return p;
+    }
+    void check_guards(cudaStream_t st) {
+        if (guards.empty()) return;
+        std::vector<unsigned char> h(kGuardBytes);
+        ck(cudaStreamSynchronize(st), "cudaStreamSynchronize(guards)");
+        for (size_t i = 0; i < guards.size(); ++i) {
+            ck(cudaMemcpy(h.data(), guards[i], kGuardBytes, cudaMemcpyDeviceToHost), "cudaMemcpy(guard)");
+            for (unsigned char c : h)
+                if (c != kGuardByte)
+                    throw RuntimeError("debug guard: workspace region " + std::to_string(i) + " was overrun");
+        }
     }
     ~Arena() {
         if (base) cudaFreeAsync(base, s);
@@ -519,7 +545,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
         J = std::max(J, int(P.lv.size()) - P.nc);
     }
     Arena W;
-    W.reserve(ws, s);
+    W.reserve(ws, s, 5 * plans.size() + 1);
     for (auto& P : plans) carve(P, W);
 
     JobStage st;
@@ -786,7 +812,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
     }
 
     Arena B;
-    B.reserve(al(st.host.size()) + al(std::max<size_t>(st.counters, 1) * sizeof(unsigned)), s);
+    B.reserve(al(st.host.size()) + al(std::max<size_t>(st.counters, 1) * sizeof(unsigned)), s, 2);
     unsigned char* djobs = B.take<unsigned char>(st.host.size());
     unsigned* dctr = B.take<unsigned>(std::max<size_t>(st.counters, 1));
     ck(cudaMemsetAsync(dctr, 0, std::max<size_t>(st.counters, 1) * sizeof(unsigned), s), "cudaMemsetAsync");
@@ -901,6 +927,10 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             ck(cudaStreamWaitEvent(caller, ev_main, 0), "cudaStreamWaitEvent");
         }
         s = caller;
+    }
+    if (g_debug_guards) {
+        W.check_guards(s);
+        B.check_guards(s);
     }
 }
 
@@ -1314,6 +1344,7 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
 
 void fgm_set_sweep_mode(int mode) { g_sweep_mode = (mode >= 0 && mode <= 3) ? mode : 0; }
 void fgm_set_pyramid_mode(int fused) { g_pyramid_mode = fused ? 1 : 0; }
+void fgm_set_debug_guards(int on) { fgm::g_debug_guards = on ? 1 : 0; }
 
 void fgm_profile_enable(int on) {
     std::lock_guard<std::mutex> g(g_prof_mu);

@@ -520,3 +520,29 @@ def test_no_writes_outside_outputs(fgm, cuda, oracle_mod, iters_high):
         assert bool(((f >= 0) & (f <= 1)).all()) and bool(((b >= 0) & (b <= 1)).all())
     for x, y in zip(before, imgs + alps):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("iters_high", [2, 3, 8])
+def test_workspace_guards(fgm, cuda, oracle_mod, iters_high):
+    # guard bands after every workspace region (level I/alpha pyramid, pass
+    # buffers, boundary streams, job descriptors) survive a batch of ragged
+    # sizes; results are unchanged by the guard layout
+    from paper_2006_14970_b200 import synth
+
+    sizes = [(1, 1), (7, 3), (33, 65), (257, 129), (1000, 33), (2, 700), (700, 2), (3000, 70), (513, 511)]
+    imgs, alps = [], []
+    for i, (w, h) in enumerate(sizes):
+        im, al = synth.make_composite(w, h, 1300 + i, 3, 3.0)
+        imgs.append(im.to(cuda))
+        alps.append(al.to(cuda))
+    p = params_from(fgm, oracle_mod.Params(iters_high=iters_high))
+    ref = fgm.batch_solve_cuda(imgs, alps, p)
+    try:
+        fgm.set_debug_guards(1)
+        got = fgm.batch_solve_cuda(imgs, alps, p)
+        single = [fgm.ml_foreground_background_cuda(im, al, p) for im, al in zip(imgs, alps)]
+    finally:
+        fgm.set_debug_guards(0)
+    for (fa, ba), (fb, bb), (fc, bc) in zip(ref, got, single):
+        assert torch.equal(fa, fb) and torch.equal(ba, bb)
+        assert torch.equal(fa, fc) and torch.equal(ba, bc)
