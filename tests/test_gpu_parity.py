@@ -546,3 +546,33 @@ def test_workspace_guards(fgm, cuda, oracle_mod, iters_high):
     for (fa, ba), (fb, bb), (fc, bc) in zip(ref, got, single):
         assert torch.equal(fa, fb) and torch.equal(ba, bb)
         assert torch.equal(fa, fc) and torch.equal(ba, bc)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_sizes_and_params_vs_oracle(fgm, cuda, orc, oracle_mod, seed):
+    # seeded random shapes (1..320 per side, incl. 1-wide/1-high) and
+    # parameters (omega, eps_r, threshold, iteration counts 1..6) against the
+    # fp64 oracle, as a batch (level-synchronous across different schedules)
+    # and one by one
+    from paper_2006_14970_b200 import synth
+
+    rng = np.random.default_rng(20061497 + seed)
+    cases = []
+    for i in range(6):
+        w, h = (int(v) for v in rng.integers(1, 321, size=2))
+        if i == 0:
+            w = 1
+        if i == 1:
+            h = 1
+        im, al = synth.make_composite(w, h, 1400 + 10 * seed + i, 3, float(rng.uniform(1.0, 6.0)))
+        cases.append((im, al))
+    p = oracle_mod.Params(omega=float(rng.choice([0.1, 0.5, 1.0, 2.0])), eps_r=float(rng.choice([1e-5, 1e-3, 5e-3])),
+                          low_res_threshold=int(rng.choice([4, 16, 32, 64])), iters_low=int(rng.integers(1, 7)),
+                          iters_high=int(rng.integers(1, 7)))
+    outs = fgm.batch_solve_cuda([c[0].to(cuda) for c in cases], [c[1].to(cuda) for c in cases], params_from(fgm, p))
+    for (im, al), (f, b) in zip(cases, outs):
+        of, ob = orc.ml_solve(im.double().numpy(), al.double().numpy(), p)
+        assert_close("fg", f.double().cpu().numpy(), of)
+        assert_close("bg", b.double().cpu().numpy(), ob)
+        f1, b1 = gpu_solve(fgm, cuda, im.numpy(), al.numpy(), p)
+        assert np.array_equal(f1, f.double().cpu().numpy()) and np.array_equal(b1, b.double().cpu().numpy())
