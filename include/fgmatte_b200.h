@@ -36,7 +36,10 @@
  * throws std::invalid_argument (same message text, fgm_last_error());
  * FGM_RUNTIME_ERROR (2) for CUDA / runtime failures.  There is no CPU
  * fallback: without a usable sm_100 device every solve returns 2.
- * fgm_last_error() is thread-local.  All entry points are reentrant.
+ * fgm_last_error() is thread-local.  The solve entry points are reentrant
+ * (concurrent calls on distinct buffers and streams are safe, from any host
+ * thread and for any current device); the fgm_set_* / fgm_debug_* / profiling
+ * switches below are process-wide settings (atomic) meant for tests and tools.
  */
 #ifndef FGMATTE_B200_H
 #define FGMATTE_B200_H
@@ -132,17 +135,25 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
                          int h, int iterations, double regularization, double gradient_weight, float* fg_out,
                          float* bg_out, void* stream);
 
-/* Big-level sweep kernel choice (tuning): 0 = automatic (per-(band, channel)
- * warps, rank-one form of the 2x2 solve), 1 = the same kernel,
- * 2 = full-channel warps (coefficients once per pixel, handed down by shuffle),
- * 3 = band CTAs: three channel warps fed by one coefficient warp (K <= 2).
- * Modes 2 and 3 use the adjugate form (bitwise equal to each other) and agree
- * with mode 0/1 within the fp32 tolerance. */
-void fgm_set_sweep_mode(int mode);
-/* Tuning/debug: 1 computes the I/alpha pyramid of all sub-top levels in one
- * pass over the full-res input (pyramid_kernel), 0 (default) with one resample
- * launch per level (image.cpp:114-133 each).  Both are bitwise identical. */
+/* Tuning/debug (process-wide, atomic): 1 computes the I/alpha pyramid of all
+ * sub-top levels in one pass over the full-res input (pyramid_kernel), 0
+ * (default) with one resample launch per level (image.cpp:114-133 each).  Both
+ * are bitwise identical. */
 void fgm_set_pyramid_mode(int fused);
+
+/* Failure detection.  A big-level sweep band waits for the band above
+ * through a boundary stream; every such wait is bounded (default 2000 ms,
+ * fgm_set_spin_timeout_ms).  A wait that times out aborts its launch (every
+ * other waiter of the launch gives up at once), increments a per-device fault
+ * counter, and makes the synchronous (host-buffer) entry points return
+ * FGM_RUNTIME_ERROR.  fgm_device_faults() synchronises the current device and
+ * returns the counter (reset != 0 clears it), or -FGM_RUNTIME_ERROR.
+ * fgm_debug_fault(1) makes band 0 of every sweep skip publishing its boundary
+ * stream (a deliberate hand-over fault for tests); 0 turns it off.  These three
+ * settings are process-wide and atomic. */
+void fgm_set_spin_timeout_ms(int ms);
+int fgm_device_faults(int reset);
+void fgm_debug_fault(int code);
 
 /* Debug: 1 surrounds every workspace region of a solve with a guard band and
  * checks it (synchronously) when the solve's work is done; an overrun fails

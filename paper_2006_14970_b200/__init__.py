@@ -116,9 +116,11 @@ def _load():
     L.fgm_sweep_passes_f32.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp, vp,
                                        vp]
     L.fgm_profile_enable.argtypes = [C.c_int]
-    L.fgm_set_sweep_mode.argtypes = [C.c_int]
     L.fgm_set_pyramid_mode.argtypes = [C.c_int]
     L.fgm_set_debug_guards.argtypes = [C.c_int]
+    for name in ("fgm_debug_fault", "fgm_set_spin_timeout_ms", "fgm_device_faults"):
+        if hasattr(L, name):  # (absent from older builds loaded through FGMATTE_B200_LIB by tools/)
+            getattr(L, name).argtypes = [C.c_int]
     L.fgm_kernel_stats.argtypes = [C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]
     L.fgm_profile_timeline.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -139,11 +141,6 @@ def device_count() -> int:
     return int(_load().fgm_device_count())
 
 
-def set_sweep_mode(mode: int) -> None:
-    """0 automatic, 1 per-(band, channel) warps, 2 full-channel warps."""
-    _load().fgm_set_sweep_mode(int(mode))
-
-
 def set_pyramid_mode(fused: int) -> None:
     """1 fused I/alpha pyramid, 0 (default) one resample launch per level."""
     _load().fgm_set_pyramid_mode(int(fused))
@@ -152,6 +149,24 @@ def set_pyramid_mode(fused: int) -> None:
 def set_debug_guards(on: int) -> None:
     """1: guard bands around every workspace region, checked after each solve."""
     _load().fgm_set_debug_guards(int(on))
+
+
+def set_spin_timeout_ms(ms: int) -> None:
+    """Bound on one boundary-stream wait of the big-level sweep (default 2000 ms)."""
+    _load().fgm_set_spin_timeout_ms(int(ms))
+
+
+def debug_fault(code: int) -> None:
+    """Fault injection for tests: 1 = band 0 of every sweep skips publishing its stream."""
+    _load().fgm_debug_fault(int(code))
+
+
+def device_faults(reset: bool = False) -> int:
+    """Synchronise the current device; the count of timed-out sweep waits."""
+    n = _load().fgm_device_faults(1 if reset else 0)
+    if n < 0:
+        _check(-n)
+    return n
 
 
 def version() -> str:

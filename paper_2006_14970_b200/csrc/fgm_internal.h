@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 namespace fgm {
 
 // ---- K1/K2: bilinear resample (image.cpp:71-133) --------------------------
@@ -89,19 +91,9 @@ inline int sweep_bands(int h, int K) { return (h + K - 1 + kBandRows - 1) / kBan
 __host__ __device__ inline size_t sweep_stream_len(int w, int K) {
     return (size_t(w + K - 1) * size_t(K) * 2 + 3) / 4 * 4;
 }
-// Streams of the full-channel kernel (sweep_full.cu): per column the K x 3
-// (F, B) pairs and the (K-1) passed 13-float coefficient sets, each part
-// padded to 16 bytes.
-__host__ __device__ inline size_t sweep_full_stream_len(int w, int K) {
-    return size_t(w + K - 1) * size_t((6 * K + 3) / 4 * 4 + (13 * (K - 1) + 3) / 4 * 4);
-}
-inline size_t sweep_full_stream_floats(int w, int h, int K) {
-    return size_t(sweep_bands(h, K)) * sweep_full_stream_len(w, K);
-}
 inline size_t sweep_stream_floats(int w, int h, int K) {
     return size_t(sweep_bands(h, K)) * 3 * sweep_stream_len(w, K);
 }
-
 // Launch helpers (kernels.cu).  `jobs_dev` are device copies of the arrays.
 // Tiles of 128 x 8 destination pixels; total_tiles = sum over jobs.
 int resample_tiles(int dw, int dh);
@@ -122,20 +114,15 @@ cudaError_t launch_compose(const float* fg, const float* bg, const float* alpha,
                            cudaStream_t s);  // scale within the staged window
 cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float omega, cudaStream_t s);
 // order_dev[t] = (job, 3 * band + channel) of ticket t, band-major across jobs.
-cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands, unsigned* ticket,
-                         float eps, float omega, cudaStream_t s);
-// Fill every job's boundary streams with kStreamSentinel (before its sweep);
-// full = the stream format of launch_sweep_full.
-cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, bool full, size_t max_floats,
-                               cudaStream_t s);
-// The full-channel (throughput) sweep kernel, same contract as launch_sweep;
-// order_dev holds (job, band) pairs.
-// band-CTA kernel (sweep_cta.cu): one ticket per band, per-channel streams
-int sweep_cta_supported_k(int K);
-cudaError_t launch_sweep_cta(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands,
-                             unsigned* ticket, float eps, float omega, cudaStream_t s);
-cudaError_t launch_sweep_full(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_bands,
-                              unsigned* ticket, float eps, float omega, cudaStream_t s);
+// ticket: the launch's zeroed ticket counter; abort_flag: a zeroed per-launch
+// int (a timed-out boundary-stream wait sets it and every waiter gives up);
+// fault_count: a persistent per-device counter of timed-out waits.
+cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
+                         float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
+extern std::atomic<int> g_sweep_fault;            // debug fault injection (fgm_debug_fault)
+extern std::atomic<long long> g_spin_timeout_ns;  // bound on one boundary-stream wait
+// Fill every job's boundary streams with kStreamSentinel (before its sweep).
+cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, size_t max_floats, cudaStream_t s);
 cudaError_t launch_f64_to_f32(const double* src, float* dst, size_t n, cudaStream_t s);
 cudaError_t launch_f32_to_f64(const float* src, double* dst, size_t n, cudaStream_t s);
 size_t coarse_smem_bytes();

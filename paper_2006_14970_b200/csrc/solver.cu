@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -225,7 +226,7 @@ int vec4_ok(const SweepJob& j) {
 // a guard of kGuardBytes filled with a byte pattern; check_guards() (called at
 // the end of a solve, synchronously) fails the call if a kernel wrote past a
 // region (level buffers, pass ping-pong, boundary streams, job descriptors).
-int g_debug_guards = 0;
+std::atomic<int> g_debug_guards{0};
 constexpr size_t kGuardBytes = 4096;
 constexpr unsigned char kGuardByte = 0xA5;
 
@@ -234,15 +235,17 @@ struct Arena {
     size_t size = 0, off = 0;
     cudaStream_t s = nullptr;
     std::vector<char*> guards;
+    bool guarded_ = false;  // guard mode latched at reserve()
     void reserve(size_t bytes, cudaStream_t st, size_t max_takes = 8) {
         s = st;
-        size = bytes + (g_debug_guards ? max_takes * kGuardBytes : 0);
+        guarded_ = g_debug_guards.load() != 0;
+        size = bytes + (guarded_ ? max_takes * kGuardBytes : 0);
         if (size) ck(cudaMallocAsync(reinterpret_cast<void**>(&base), size, s), "cudaMallocAsync");
     }
     template <class T>
     T* take(size_t count) {
         const size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
-        const size_t gb = g_debug_guards ? kGuardBytes : 0;
+        const size_t gb = guarded_ ? kGuardBytes : 0;
         if (off + bytes + gb > size) throw RuntimeError("internal: arena overflow");
         T* p = reinterpret_cast<T*>(base + off);
         off += bytes;
@@ -315,9 +318,7 @@ void plan_image(Plan& P, const fgm_params* p) {
         }
         if (l >= P.nc) {
             for (int K : passes_for(P.lv[size_t(l)].iters)) {
-                P.stream_floats = std::max(P.stream_floats,
-                                           std::max(sweep_stream_floats(P.lv[size_t(l)].w, P.lv[size_t(l)].h, K),
-                                                    sweep_full_stream_floats(P.lv[size_t(l)].w, P.lv[size_t(l)].h, K)));
+                P.stream_floats = std::max(P.stream_floats, sweep_stream_floats(P.lv[size_t(l)].w, P.lv[size_t(l)].h, K));
                 P.max_bands = std::max(P.max_bands, sweep_bands(P.lv[size_t(l)].h, K));
             }
             if (passes_for(P.lv[size_t(l)].iters).size() > 1) P.multipass = true;
@@ -398,7 +399,6 @@ struct JobStage {
 // Ticket order of a sweep launch: band-major across its jobs, so that the
 // bands running at any moment belong to many images (no pipeline fill per
 // image) and every band's predecessor has a smaller ticket.
-// full: one item per band (full-channel kernel); else one per (band, channel).
 // Ticket order of a launch's bands: critical path first.  Band q of image i
 // can start ~q*lag steps after the image's band 0 (the boundary-stream lag of
 // 32 rows + a 16-column chunk) and the image's chain ends (nb-1)*lag + w steps
@@ -406,7 +406,7 @@ struct JobStage {
 // tickets follow S_i + q*lag.  Within an image the order is q ascending (an
 // awaited band always holds an earlier ticket: no deadlock); the tall/wide
 // images' long chains start first instead of forming the launch's tail.
-std::vector<int2> band_order(const std::vector<SweepJob>& sj, bool full) {
+std::vector<int2> band_order(const std::vector<SweepJob>& sj) {
     constexpr double lag = kBandRows + kChunk;
     struct Key {
         double k;
@@ -419,49 +419,49 @@ std::vector<int2> band_order(const std::vector<SweepJob>& sj, bool full) {
     }
     std::stable_sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) { return a.k < b.k; });
     std::vector<int2> ord;
-    ord.reserve(keys.size() * (full ? 1 : 3));
-    for (const Key& k : keys) {
-        if (full)
-            ord.push_back(make_int2(k.i, k.q));
-        else
-            for (int c = 0; c < 3; ++c) ord.push_back(make_int2(k.i, 3 * k.q + c));
-    }
+    ord.reserve(keys.size() * 3);
+    for (const Key& k : keys)
+        for (int c = 0; c < 3; ++c) ord.push_back(make_int2(k.i, 3 * k.q + c));
     return ord;
 }
 
-// Kernel choice per sweep launch: 0 per-(band, channel) warps (sweep.cu),
-// 1 full-channel warps (sweep_full.cu), 2 band CTAs with a shared
-// coefficient warp (sweep_cta.cu).  All three are bitwise identical.
-int g_sweep_mode = 0;  // 0 auto, 1 per-channel, 2 full-channel, 3 band CTA
-// 1: fused I/alpha pyramid (pyramid_kernel), 0: one resample launch per level
-// (FGM_PYRAMID in the environment sets the initial value)
-int g_pyramid_mode = [] {  // default per level: the fused pass measured slower
-    const char* e = std::getenv("FGM_PYRAMID");
-    return e ? (std::atoi(e) != 0 ? 1 : 0) : 0;
-}();
-int sweep_kind(int total_bands, int K) {
-    (void)total_bands;
-    if (g_sweep_mode == 2 && K <= 3) return 1;  // the full-channel kernel's state does not fit beyond K = 3
-    if (g_sweep_mode == 3 && sweep_cta_supported_k(K)) return 2;
-    return 0;
-}
-// one ticket per band (kinds 1, 2) or per (band, channel) (kind 0)
-inline bool per_band(int kind) { return kind != 0; }
+// 1: fused I/alpha pyramid (pyramid_kernel), 0 (default): one resample launch
+// per level; the fused pass measured slower
+std::atomic<int> g_pyramid_mode{0};
 
-cudaError_t launch_sweep_kind(int kind, int K, const SweepJob* jd, const int2* od, int bands, unsigned* ticket,
-                              float eps, float omega, cudaStream_t s) {
-    switch (kind) {
-        case 1: return launch_sweep_full(K, jd, od, bands, ticket, eps, omega, s);
-        case 2: return launch_sweep_cta(K, jd, od, bands, ticket, eps, omega, s);
-        default: return launch_sweep(K, jd, od, 3 * bands, ticket, eps, omega, s);
+// Persistent per-device count of timed-out boundary-stream waits (sweep.cu).
+int* device_fault_counter() {
+    constexpr int kMaxDev = 64;
+    static std::mutex mu;
+    static int* ctr[kMaxDev] = {};
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= kMaxDev) throw RuntimeError("device index out of range");
+    std::lock_guard<std::mutex> g(mu);
+    if (!ctr[dev]) {
+        ck(cudaMalloc(reinterpret_cast<void**>(&ctr[dev]), sizeof(int)), "cudaMalloc(fault counter)");
+        ck(cudaMemset(ctr[dev], 0, sizeof(int)), "cudaMemset(fault counter)");
     }
+    return ctr[dev];
+}
+
+int read_faults() {
+    int v = 0;
+    ck(cudaMemcpy(&v, device_fault_counter(), sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(fault counter)");
+    return v;
+}
+
+// ticket[0]: the launch's band ticket, ticket[1]: its abort flag (both zeroed)
+cudaError_t launch_sweep_passes(int K, const SweepJob* jd, const int2* od, int bands, unsigned* ticket, float eps,
+                                float omega, cudaStream_t s) {
+    return launch_sweep(K, jd, od, 3 * bands, ticket, eps, omega, reinterpret_cast<int*>(ticket + 1),
+                        device_fault_counter(), s);
 }
 
 enum LaunchKind { kCoarse, kResample, kUpsample, kSweep, kCopy, kPyramid };
 struct LaunchRec {
     LaunchKind kind;
     int K, njobs, total_bands;
-    int skind;  // sweep kernel kind (sweep_kind)
     size_t job_off, ticket, order_off;
     long long max_rows;
     double bytes;
@@ -476,21 +476,8 @@ struct LaunchRec {
 // upsamples and sweeps), and a pool of events.
 struct SideStream {
     int dev = -1;
-    int prio_hi = 0;
     cudaStream_t s = nullptr;
     std::vector<cudaEvent_t> ev;
-    // high-priority twins of the caller's streams: the main work of a solve
-    // runs there, so the scheduler hands freed SM slots to its blocks before
-    // the pyramid's (a caller stream has the default, lowest, priority)
-    std::vector<std::pair<cudaStream_t, cudaStream_t>> hi;
-    cudaStream_t high(cudaStream_t caller) {
-        for (auto& h : hi)
-            if (h.first == caller) return h.second;
-        cudaStream_t t;
-        ck(cudaStreamCreateWithPriority(&t, cudaStreamNonBlocking, prio_hi), "cudaStreamCreate");
-        hi.emplace_back(caller, t);
-        return t;
-    }
     cudaEvent_t event(size_t i) {
         while (ev.size() <= i) {
             cudaEvent_t e;
@@ -501,16 +488,8 @@ struct SideStream {
     }
 };
 thread_local SideStream g_side;
-#ifndef FGM_SIDE_BLOCKS
-#define FGM_SIDE_BLOCKS 16
-#endif
-int side_blocks_per_sm() {  // (tuning knob FGM_SIDE_BLOCKS_RT overrides; 0 = one tile per block)
-    static const int v = [] {
-        const char* e = std::getenv("FGM_SIDE_BLOCKS_RT");
-        return e ? std::atoi(e) : FGM_SIDE_BLOCKS;
-    }();
-    return v;
-}
+// persistent blocks per SM of the side-stream pyramid launches (16 fills the GPU)
+constexpr int kSideBlocksPerSm = 16;
 
 SideStream& side_stream() {
     int dev = 0;
@@ -519,10 +498,7 @@ SideStream& side_stream() {
         g_side = SideStream{};
         int lo = 0, hi = 0;  // lowest priority: its blocks yield SM slots to the main stream's
         ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
-        const char* e = std::getenv("FGM_SIDE_HI");  // (tuning knob: pyramid at the highest priority)
-        ck(cudaStreamCreateWithPriority(&g_side.s, cudaStreamNonBlocking, e && std::atoi(e) ? hi : lo),
-           "cudaStreamCreate");
-        g_side.prio_hi = hi;
+        ck(cudaStreamCreateWithPriority(&g_side.s, cudaStreamNonBlocking, lo), "cudaStreamCreate");
         g_side.dev = dev;
     }
     return g_side;
@@ -587,7 +563,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             c.out_pstride = (long long)c.out_pitch * Lc.h;
             bytes += 24.0 * double(n);
         }
-        launches.push_back({kCoarse, 0, int(cj.size()), 0, false, st.push(cj), 0, 0, 0, bytes});
+        launches.push_back({kCoarse, 0, int(cj.size()), 0, st.push(cj), 0, 0, 0, bytes});
     }
 
     // ---- I/alpha pyramid of every big sub-top level, on the side stream ----
@@ -595,7 +571,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
     // (pyramid_kernel); its event (index J + 3) gates the first sweep of
     // every sub-top level.  Per level (FGM_PYRAMID=0): step j's resample
     // launch records event j and step j's sweep waits for it.
-    const bool fused_pyr = g_pyramid_mode != 0;
+    const bool fused_pyr = g_pyramid_mode.load() != 0;
     bool pyr_fits = true;
     for (const auto& P : plans) pyr_fits = pyr_fits && int(P.lv.size()) - 1 - P.nc <= kMaxPyr;
     const int pyr_ev = J + 3;
@@ -632,21 +608,13 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             pj.push_back(q);
         }
         if (!pj.empty()) {
-            LaunchRec lr{kPyramid, 0, int(pj.size()), 0, false, st.push(pj), 0, 0, tiles, bytes};
+            LaunchRec lr{kPyramid, 0, int(pj.size()), 0, st.push(pj), 0, 0, tiles, bytes};
             lr.side = 1;
             lr.ev = pyr_ev;
             launches.push_back(lr);
             pyr_launch = true;
         }
     }
-    // (tuning knob FGM_PYR_LAST_MAIN=1: the largest level's I/alpha runs on the
-    // main stream right before that level instead of beside the small levels)
-    static const bool pyr_last_main = [] {
-        const char* e = std::getenv("FGM_PYR_LAST_MAIN");
-        return e && std::atoi(e) != 0;
-    }();
-    LaunchRec last_pyr{};
-    bool has_last_pyr = false;
     for (int j = 0; j < J && !pyr_launch; ++j) {
         std::vector<ResampleJob> rj;
         long long tiles = 0;
@@ -669,12 +637,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             r.tile_base = int(tiles);
             tiles += resample_tiles(r.dw, r.dh);
         }
-        LaunchRec lr{kResample, 0, int(rj.size()), 0, false, st.push(rj), 0, 0, tiles, rbytes};
-        if (pyr_last_main && j == J - 2) {  // runs on the main stream just before its level
-            last_pyr = lr;
-            has_last_pyr = true;
-            continue;
-        }
+        LaunchRec lr{kResample, 0, int(rj.size()), 0, st.push(rj), 0, 0, tiles, rbytes};
         lr.side = 1;
         lr.ev = j;
         launches.push_back(lr);
@@ -685,7 +648,6 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
 
     // ---- big levels, aligned so that every image's top level is step J-1 --
     for (int j = 0; j < J; ++j) {
-        if (has_last_pyr && j == J - 2) launches.push_back(last_pyr);
         std::vector<ResampleJob> rj, uj;  // resample (I/alpha) and upsample (F/B) jobs
         long long max_rows = 0;
         double rbytes = 0, ubytes = 0;
@@ -719,13 +681,13 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             r.tile_base = int(max_rows);
             max_rows += resample_tiles(r.dw, r.dh);
         }
-        if (!rj.empty()) launches.push_back({kResample, 0, int(rj.size()), 0, false, st.push(rj), 0, 0, max_rows, rbytes});
+        if (!rj.empty()) launches.push_back({kResample, 0, int(rj.size()), 0, st.push(rj), 0, 0, max_rows, rbytes});
         long long up_tiles = 0;
         for (auto& r : uj) {
             r.tile_base = int(up_tiles);
             up_tiles += upsample_tiles(r.dw, r.dh);
         }
-        if (!uj.empty()) launches.push_back({kUpsample, 0, int(uj.size()), 0, false, st.push(uj), 0, 0, up_tiles, ubytes});
+        if (!uj.empty()) launches.push_back({kUpsample, 0, int(uj.size()), 0, st.push(uj), 0, 0, up_tiles, ubytes});
         size_t max_passes = 0;
         for (auto& a : act) max_passes = std::max(max_passes, passes_for(a.P->lv[size_t(a.l)].iters).size());
         for (size_t pi = 0; pi < max_passes; ++pi) {
@@ -734,7 +696,8 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 int total = 0;
                 double sbytes = 0;
                 size_t max_stream = 0;
-                const size_t ticket = st.counters++;
+                const size_t ticket = st.counters;
+                st.counters += 2;  // ticket, abort flag
                 for (auto& a : act) {
                     Plan& P = *a.P;
                     const std::vector<int> ps = passes_for(P.lv[size_t(a.l)].iters);
@@ -777,19 +740,17 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                     J1.band_base = total;
                     J1.vec4 = vec4_ok(J1);
                     total += J1.nb;
-                    max_stream = std::max(max_stream, std::max(sweep_stream_floats(L.w, L.h, K),
-                                                               sweep_full_stream_floats(L.w, L.h, K)));
+                    max_stream = std::max(max_stream, sweep_stream_floats(L.w, L.h, K));
                     sbytes += 64.0 * double(px);
                     sj.push_back(J1);
                 }
                 if (sj.empty()) {
-                    --st.counters;
+                    st.counters -= 2;
                     continue;
                 }
-                const int sk = sweep_kind(total, K);
                 const size_t off = st.push(sj);
-                const size_t ooff = st.push(band_order(sj, per_band(sk)));
-                LaunchRec lr{kSweep, K, int(sj.size()), total, sk, off, ticket, ooff, (long long)max_stream, sbytes};
+                const size_t ooff = st.push(band_order(sj));
+                LaunchRec lr{kSweep, K, int(sj.size()), total, off, ticket, ooff, (long long)max_stream, sbytes};
                 if (pi == 0 && has_ia[size_t(j)]) lr.ev = j;  // this step's I/alpha pyramid level
                 if (pi == 0 && pyr_launch && j < J - 1) lr.ev = pyr_ev;
                 launches.push_back(lr);
@@ -805,9 +766,9 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             const float* b = top ? P.io.bg : P.fbOut + 3 * size_t(sp) * L.h;
             // 3 planes = 3h rows of the source pitch (plane stride = pitch * h)
             if (P.io.level_fg[a.l])
-                launches.push_back({kCopy, 0, L.w, 3 * L.h, false, 0, 0, 0, sp, 0.0, P.io.level_fg[a.l], f});
+                launches.push_back({kCopy, 0, L.w, 3 * L.h, 0, 0, 0, sp, 0.0, P.io.level_fg[a.l], f});
             if (P.io.level_bg[a.l])
-                launches.push_back({kCopy, 0, L.w, 3 * L.h, false, 0, 0, 0, sp, 0.0, P.io.level_bg[a.l], b});
+                launches.push_back({kCopy, 0, L.w, 3 * L.h, 0, 0, 0, sp, 0.0, P.io.level_bg[a.l], b});
         }
     }
 
@@ -819,48 +780,30 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
     g_pinned.stage(st.host.data(), st.host.size(), s, djobs);
 
     // the side stream starts after everything enqueued on s so far (inputs,
-    // job uploads) and s waits for all of its work at the end
+    // job uploads) and s waits for all of its work at the end -- also when a
+    // launch below throws: the join is a scope guard declared after the
+    // arenas, so it runs before their stream-ordered frees
     SideStream& side = side_stream();
     const cudaEvent_t ev_start = side.event(size_t(J)), ev_end = side.event(size_t(J) + 1);
-    // (tuning knob FGM_PYRAMID_MAIN=1: the I/alpha pyramid runs first, on the
-    // main stream, instead of overlapping the coarse and small levels)
-    static const bool pyr_main = [] {
-        const char* e = std::getenv("FGM_PYRAMID_MAIN");
-        return e && std::atoi(e) != 0;
-    }();
     bool any_side = false;
     for (const LaunchRec& r : launches) any_side = any_side || r.side;
-    any_side = any_side && !pyr_main;
-    // tuning knob FGM_MAIN_HI=1: main work on the caller stream's high-priority twin
-    static const bool main_hi = [] {  // (default off: measured neutral on the C4 batch)
-        const char* e = std::getenv("FGM_MAIN_HI");
-        return e && std::atoi(e) != 0;
-    }();
-    const cudaStream_t caller = s;
+    struct SideJoin {
+        bool armed = false;
+        cudaStream_t side, caller;
+        cudaEvent_t ev;
+        ~SideJoin() {
+            if (!armed) return;
+            cudaEventRecord(ev, side);
+            cudaStreamWaitEvent(caller, ev, 0);
+        }
+    } join{false, side.s, s, ev_end};
     if (any_side) {
         ck(cudaEventRecord(ev_start, s), "cudaEventRecord");
         ck(cudaStreamWaitEvent(side.s, ev_start, 0), "cudaStreamWaitEvent");
-        if (main_hi) {
-            s = side.high(caller);
-            ck(cudaStreamWaitEvent(s, ev_start, 0), "cudaStreamWaitEvent");
-        }
+        join.armed = true;
     }
 
-    if (pyr_main) {
-        for (const LaunchRec& r : launches) {
-            if (!r.side) continue;
-            ProfScope ps(s, 1, r.bytes);
-            if (r.kind == kPyramid)
-                ck(launch_pyramid(reinterpret_cast<const PyrJob*>(djobs + r.job_off), r.njobs, r.max_rows, s),
-                   "pyramid_kernel");
-            else
-                ck(launch_resample(reinterpret_cast<const ResampleJob*>(djobs + r.job_off), r.njobs, r.max_rows, s),
-                   "resample_kernel");
-        }
-    }
-    for (const LaunchRec& r0 : launches) {
-        const LaunchRec& r = r0;
-        if (r.side && pyr_main) continue;
+    for (const LaunchRec& r : launches) {
         if (r.side && r.kind == kPyramid) {  // the whole I/alpha pyramid
             ProfScope ps(side.s, 1, r.bytes);
             ck(launch_pyramid(reinterpret_cast<const PyrJob*>(djobs + r.job_off), r.njobs, r.max_rows, side.s),
@@ -871,12 +814,12 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
         if (r.side) {  // I/alpha pyramid level
             ProfScope ps(side.s, 1, r.bytes);
             ck(launch_resample(reinterpret_cast<const ResampleJob*>(djobs + r.job_off), r.njobs, r.max_rows, side.s,
-                               side_blocks_per_sm()),
+                               kSideBlocksPerSm),
                "resample_kernel");
             ck(cudaEventRecord(side.event(size_t(r.ev)), side.s), "cudaEventRecord");
             continue;
         }
-        if (r.ev >= 0 && !pyr_main) ck(cudaStreamWaitEvent(s, side.event(size_t(r.ev)), 0), "cudaStreamWaitEvent");
+        if (r.ev >= 0) ck(cudaStreamWaitEvent(s, side.event(size_t(r.ev)), 0), "cudaStreamWaitEvent");
         switch (r.kind) {
             case kPyramid: break;  // (side stream only)
             case kCoarse: {
@@ -898,17 +841,13 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 break;
             }
             case kSweep: {
-                ck(launch_stream_fill(reinterpret_cast<const SweepJob*>(djobs + r.job_off), r.njobs, r.K, r.skind == 1,
+                ck(launch_stream_fill(reinterpret_cast<const SweepJob*>(djobs + r.job_off), r.njobs, r.K,
                                       size_t(r.max_rows), s),
                    "stream_fill_kernel");
-                if (std::getenv("FGM_DEBUG_SWEEP"))
-                    std::fprintf(stderr, "[fgm] sweep K=%d jobs=%d bands=%d kind=%d\n", r.K, r.njobs, r.total_bands,
-                                 r.skind);
                 ProfScope ps(s, 0, r.bytes);
                 const SweepJob* jd = reinterpret_cast<const SweepJob*>(djobs + r.job_off);
                 const int2* od = reinterpret_cast<const int2*>(djobs + r.order_off);
-                ck(launch_sweep_kind(r.skind, r.K, jd, od, r.total_bands, dctr + r.ticket, eps, omega, s),
-                   "sweep_kernel");
+                ck(launch_sweep_passes(r.K, jd, od, r.total_bands, dctr + r.ticket, eps, omega, s), "sweep_kernel");
                 break;
             }
             case kCopy:  // njobs = width, total_bands = rows, max_rows = source pitch (floats)
@@ -919,16 +858,11 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
         }
     }
     if (any_side) {  // nothing of this call stays outstanding on the side stream
+        join.armed = false;
         ck(cudaEventRecord(ev_end, side.s), "cudaEventRecord");
-        ck(cudaStreamWaitEvent(caller, ev_end, 0), "cudaStreamWaitEvent");
-        if (s != caller) {  // nor on the high-priority twin
-            const cudaEvent_t ev_main = side.event(size_t(J) + 2);
-            ck(cudaEventRecord(ev_main, s), "cudaEventRecord");
-            ck(cudaStreamWaitEvent(caller, ev_main, 0), "cudaStreamWaitEvent");
-        }
-        s = caller;
+        ck(cudaStreamWaitEvent(s, ev_end, 0), "cudaStreamWaitEvent");
     }
-    if (g_debug_guards) {
+    if (W.guarded_ || B.guarded_) {
         W.check_guards(s);
         B.check_guards(s);
     }
@@ -946,6 +880,15 @@ int guarded(F&& fn) {
         g_err = e.what();
         return FGM_RUNTIME_ERROR;
     }
+}
+
+// A boundary-stream wait that timed out (a band whose predecessor never
+// published) aborts its launch; synchronous entry points report it.
+void check_faults(int before) {
+    if (read_faults() != before)
+        throw RuntimeError("sweep: a boundary-stream wait timed out after " +
+                           std::to_string(g_spin_timeout_ns.load() / 1000000) +
+                           " ms (band hand-over stalled); the launch was aborted and its results are invalid");
 }
 
 void check_dims(int w, int h) {
@@ -1037,8 +980,12 @@ static int host_solve_impl(const void* image, const void* alpha, int w, int h, c
             ~SG() { cudaStreamDestroy(s); }
         } sg{s};
         const size_t n = size_t(w) * h;
+        const int faults0 = read_faults();
         Arena A;
-        A.reserve(al(16 * n * sizeof(float)) + al(24 * n * sizeof(float)) + (f64 ? 2 * al(24 * n * sizeof(double)) : 0),
+        // image + alpha (4 planes) and F + B (6 planes) in fp32; the fp64 path
+        // stages the 4 input planes and the 6 output planes in fp64 as well
+        A.reserve(al(4 * n * sizeof(float)) + al(6 * n * sizeof(float)) +
+                      (f64 ? al(6 * n * sizeof(double)) + al(6 * n * sizeof(double)) : 0),
                   s);
         float* dimg = A.take<float>(4 * n);  // 3 image planes + alpha
         float* dout = A.take<float>(6 * n);
@@ -1062,6 +1009,7 @@ static int host_solve_impl(const void* image, const void* alpha, int w, int h, c
             ck(cudaMemcpyAsync(bg, dout + 3 * n, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, s), "D2H");
         }
         ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        check_faults(faults0);
     });
 }
 
@@ -1073,6 +1021,7 @@ int fgm_batch_solve_host_f32(int n_images, const float* const* images, const flo
         for (int i = 0; i < n_images; ++i) check_dims(widths[i], heights[i]);
         if (n_images == 0) return;
         require_device();
+        const int faults0 = read_faults();
         // Sub-batches of ~1/64 of the pixels (at least one image each) in
         // kSlots device slots: copy-in runs up to kSlots groups ahead of
         // copy-out, so both PCIe directions stay busy while the (much
@@ -1170,6 +1119,7 @@ int fgm_batch_solve_host_f32(int n_images, const float* const* images, const flo
             cudaEventDestroy(ev_done[g]);
             cudaEventDestroy(ev_out[g]);
         }
+        check_faults(faults0);
     });
 }
 
@@ -1293,7 +1243,7 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
         size_t sf = 0;
         int mb = 0;
         for (int K : ps) {
-            sf = std::max(sf, std::max(sweep_stream_floats(w, h, K), sweep_full_stream_floats(w, h, K)));
+            sf = std::max(sf, sweep_stream_floats(w, h, K));
             mb = std::max(mb, sweep_bands(h, K));
         }
         Arena A;
@@ -1321,19 +1271,17 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
             J1.nb = sweep_bands(h, ps[pi]);
             J1.band_base = 0;
             J1.vec4 = vec4_ok(J1);
-            ck(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s), "memset");
+            ck(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned), s), "memset");
             SweepJob* d = A.take<SweepJob>(1);
             ck(cudaMemcpyAsync(d, &J1, sizeof(J1), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
-            const int sk = sweep_kind(J1.nb, ps[pi]);
-            const std::vector<int2> ord = band_order({J1}, per_band(sk));
+            const std::vector<int2> ord = band_order({J1});
             int2* dord = A.take<int2>(ord.size());
             ck(cudaMemcpyAsync(dord, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice, s),
                "cudaMemcpyAsync(order)");
-            ck(launch_stream_fill(d, 1, ps[pi], sk == 1, sf, s), "stream_fill_kernel");
+            ck(launch_stream_fill(d, 1, ps[pi], sf, s), "stream_fill_kernel");
             {
                 ProfScope pr(s, 0, 64.0 * double(px));
-                ck(launch_sweep_kind(sk, ps[pi], d, dord, J1.nb, ctr, float(regularization), float(gradient_weight),
-                                     s),
+                ck(launch_sweep_passes(ps[pi], d, dord, J1.nb, ctr, float(regularization), float(gradient_weight), s),
                    "sweep_kernel");
             }
             fi = J1.fg_out;
@@ -1342,9 +1290,22 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
     });
 }
 
-void fgm_set_sweep_mode(int mode) { g_sweep_mode = (mode >= 0 && mode <= 3) ? mode : 0; }
-void fgm_set_pyramid_mode(int fused) { g_pyramid_mode = fused ? 1 : 0; }
-void fgm_set_debug_guards(int on) { fgm::g_debug_guards = on ? 1 : 0; }
+void fgm_debug_fault(int code) { fgm::g_sweep_fault.store(code); }
+
+void fgm_set_spin_timeout_ms(int ms) { fgm::g_spin_timeout_ns.store((long long)std::max(ms, 1) * 1000000ll); }
+
+int fgm_device_faults(int reset) {
+    int v = -1;
+    const int rc = guarded([&] {
+        require_device();
+        ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+        v = read_faults();
+        if (reset) ck(cudaMemset(device_fault_counter(), 0, sizeof(int)), "cudaMemset(fault counter)");
+    });
+    return rc ? -rc : v;
+}
+void fgm_set_pyramid_mode(int fused) { g_pyramid_mode.store(fused ? 1 : 0); }
+void fgm_set_debug_guards(int on) { fgm::g_debug_guards.store(on ? 1 : 0); }
 
 void fgm_profile_enable(int on) {
     std::lock_guard<std::mutex> g(g_prof_mu);

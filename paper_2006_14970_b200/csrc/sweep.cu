@@ -44,7 +44,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
+#include <atomic>
+#include <mutex>
 
 #include "fgm_device.cuh"
 #include "fgm_internal.h"
@@ -638,22 +639,57 @@ __device__ __forceinline__ bool chunk_complete(float4 q, int u0, int Umax, int l
 // Poll chunk `u0 / CK` of the band above until every word of it is
 // written; leaves it in the chunk buffer.  `v` holds a load issued earlier
 // and is re-polled only while incomplete.
+// The launch-wide failure state of a sweep: a per-launch abort flag (zeroed
+// with the ticket) and a persistent per-device fault counter.
+struct SweepFail {
+    int* abort_flag;
+    int* fault_count;
+    unsigned long long spin_ns;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Poll chunk `u0 / CK` of the band above until every word of it is
+// written; leaves it in the chunk buffer.  `v` holds a load issued earlier
+// and is re-polled only while incomplete.  Bounded (SURVEY.md section 5,
+// "timeout -> error, not a hang"): after spin_ns the wait raises the launch's
+// abort flag, counts a device fault and returns false; every other waiter of
+// the launch then gives up at once.
 template <int K, int CK>
-__device__ __forceinline__ void acquire_chunk(float4 v, const float* up_stream, int u0, int Umax, int lane,
-                                              int chunk) {
+__device__ __forceinline__ bool acquire_chunk(float4 v, const float* up_stream, int u0, int Umax, int lane,
+                                              int chunk, const SweepFail& F) {
     using G = Geom<K, CK>;
     const int nvalid = min(CK, Umax - u0) * K * 2;  // floats
     const bool mine = lane < G::CH4 && 4 * lane < nvalid;
     // (exponential back-off up to 4 us was measured: no effect on batches,
     // slower single images)
-#ifndef FGM_POLL_NS
-#define FGM_POLL_NS 32
-#endif
-    while (!__all_sync(kFull, chunk_complete<K, CK>(v, u0, Umax, lane))) {
-        if (FGM_POLL_NS) __nanosleep(FGM_POLL_NS);
+    // (the abort flag and the clock are checked every 256 polls only: a
+    // check in every poll slows the hand-over of latency-bound launches)
+    unsigned long long t0 = 0;
+    for (unsigned n = 0; !__all_sync(kFull, chunk_complete<K, CK>(v, u0, Umax, lane)); ++n) {
+        __nanosleep(32);
         if (mine) v = ld_relaxed_v4(up_stream + size_t(u0) * K * 2 + 4 * lane);
+        if ((n & 255u) == 255u) {
+            int ab = 0;
+            if (lane == 0) {
+                const unsigned long long now = global_ns();
+                if (!t0) t0 = now;
+                ab = *reinterpret_cast<volatile int*>(F.abort_flag);
+                if (!ab && now - t0 > F.spin_ns) {
+                    atomicExch(F.abort_flag, 1);
+                    atomicAdd(F.fault_count, 1);
+                    ab = 1;
+                }
+            }
+            if (__shfl_sync(kFull, ab, 0)) return false;
+        }
     }
     if (mine) sts4(chunk + 4 * lane, v);
+    return true;
 }
 
 #ifdef FGM_TRACE
@@ -670,7 +706,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 template <int K, bool V4, int CK>
 __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int lane, unsigned sbase, float eps,
-                                         float omega) {
+                                         float omega, const SweepFail& F, int fault) {
 #ifdef FGM_TRACE
     const int titem = (J.band_base + q) * 3 + ch;
     if (lane == 0 && titem < 65536) g_trace[4 * titem] = gtimer();
@@ -691,7 +727,7 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     cx.w = w;
     cx.h = h;
     cx.has_up = q > 0;
-    cx.has_down = q < J.nb - 1;
+    cx.has_down = q < J.nb - 1 && !(fault == 1 && q == 0);  // (fault 1: band 0 never publishes)
     cx.Umax = Umax;
     cx.my_stream = J.stream + size_t(sid) * slen;
     // band-relative output base (row y0 - (K-1) may be -1.. for the first
@@ -752,7 +788,11 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
             if (cx.has_up && t4 < Umax) {
                 const int nxt = (t4 & ~(CK - 1)) + CK;  // the next chunk's first column
                 if ((t4 % CK) == 0) {
-                    acquire_chunk<K, CK>(pend, up_stream, t4, Umax, lane, Gm::OFF_C);
+                    if (!acquire_chunk<K, CK>(pend, up_stream, t4, Umax, lane, Gm::OFF_C, F)) {
+                        cp_wait<0>();  // the launch is aborted: drop the band
+                        __syncwarp();
+                        return;
+                    }
 #ifdef FGM_TRACE
                     if (t4 == 0 && lane == 0 && titem < 65536) g_trace[4 * titem + 1] = gtimer();
                     if (t4 == 64 && lane == 0 && titem < 65536) g_trace[4 * titem + 2] = gtimer();
@@ -812,86 +852,103 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
 #endif
 }
 
-#ifndef FGM_SWEEP_MINB
-#define FGM_SWEEP_MINB 1  // (12 caps the K = 2 throughput kernel at 168 registers: 9 warps per SM instead of 8; measured no faster)
-#endif
+struct SweepArgs {
+    const SweepJob* jobs;
+    const int2* order;  // (job, band * 3 + channel) per ticket
+    int total;
+    unsigned* ticket;
+    float eps, omega;
+    SweepFail fail;
+    int fault;  // debug fault injection (fgm_debug_fault)
+};
+
 template <int K, bool V4, int CK>
-__global__ void __launch_bounds__(32, (K == 2 && CK >= 16) ? FGM_SWEEP_MINB : 1) sweep_kernel(const SweepJob* __restrict__ jobs, const int2* __restrict__ order,
-                                                    int total_items, unsigned* ticket, float eps, float omega) {
+__global__ void __launch_bounds__(32, 1) sweep_kernel(SweepArgs A) {
     const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sweep_sm4));
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned tk = 0;
-        if (lane == 0) tk = atomicAdd(ticket, 1u);
+        if (lane == 0) tk = atomicAdd(A.ticket, 1u);
         tk = __shfl_sync(kFull, tk, 0);
-        if (tk >= unsigned(total_items)) return;
-        const int2 jb = order[tk];  // (job, band * 3 + channel)
-        const SweepJob J = jobs[jb.x];
+        if (tk >= unsigned(A.total) || *reinterpret_cast<volatile int*>(A.fail.abort_flag)) return;
+        const int2 jb = A.order[tk];  // (job, band * 3 + channel)
+        const SweepJob J = A.jobs[jb.x];
         if (V4 && !J.vec4) {
-            run_band<K, false, CK>(J, jb.y / 3, jb.y % 3, lane, sbase, eps, omega);
+            run_band<K, false, CK>(J, jb.y / 3, jb.y % 3, lane, sbase, A.eps, A.omega, A.fail, A.fault);
         } else {
-            run_band<K, V4, CK>(J, jb.y / 3, jb.y % 3, lane, sbase, eps, omega);
+            run_band<K, V4, CK>(J, jb.y / 3, jb.y % 3, lane, sbase, A.eps, A.omega, A.fail, A.fault);
         }
     }
+}
+
+// Per-device launch state: the function attributes and the resident-warp
+// capacity are per device (a process may drive several GPUs from several
+// host threads).
+struct SweepCfg {
+    int grid_cap = 0;
+};
+template <int K, int CK>
+cudaError_t sweep_attrs(int dev) {
+    constexpr int kMaxDev = 64;
+    static std::mutex mu;
+    static bool done[kMaxDev] = {};
+    if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> g(mu);
+    if (done[dev]) return cudaSuccess;
+    const int smem = int(Geom<K, CK>::TOTAL * sizeof(float));
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<K, true, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    // the largest shared-memory carveout: the rings, not L1, bound the resident warps
+    e = cudaFuncSetAttribute(sweep_kernel<K, true, CK>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    done[dev] = true;
+    return cudaSuccess;
+}
+
+template <int K>
+cudaError_t sweep_cfg(SweepCfg& out) {
+    constexpr int kMaxDev = 64;
+    static std::mutex mu;
+    static SweepCfg cfg[kMaxDev];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+    if ((e = sweep_attrs<K, kChunk>(dev)) != cudaSuccess) return e;
+    if ((e = sweep_attrs<K, 4>(dev)) != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    if (!cfg[dev].grid_cap) {
+        int sms = 0, per_sm = 0;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<K, true, kChunk>, 32,
+                                                          size_t(Geom<K, kChunk>::TOTAL) * sizeof(float));
+        if (e != cudaSuccess) return e;
+        cfg[dev].grid_cap = std::max(1, sms * std::max(1, per_sm));
+    }
+    out = cfg[dev];
+    return cudaSuccess;
 }
 
 // Launches whose (band, channel) items all fit on the GPU at once are
 // latency-bound single images: their critical path crosses every band, one
 // boundary-stream chunk per hand-over, so they poll 4-column chunks (a ~20%
 // shorter hand-over lag); throughput launches poll 16-column chunks.
-template <int K, int CK>
-cudaError_t launch_sweep_kc(const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
-                            float eps, float omega, cudaStream_t s, int grid_cap) {
-    const size_t smem = size_t(Geom<K, CK>::TOTAL) * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(sweep_kernel<K, true, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        // the largest shared-memory carveout: the rings, not L1, bound the resident warps
-        e = cudaFuncSetAttribute(sweep_kernel<K, true, CK>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    const int grid = std::max(1, std::min(total_items, grid_cap));
-    sweep_kernel<K, true, CK><<<grid, 32, smem, s>>>(jobs_dev, order_dev, total_items, ticket, eps, omega);
+template <int K>
+cudaError_t launch_sweep_k(const SweepArgs& A, cudaStream_t s) {
+    SweepCfg c;
+    cudaError_t e = sweep_cfg<K>(c);
+    if (e != cudaSuccess) return e;
+    const int grid = std::max(1, std::min(A.total, c.grid_cap));
+    if (A.total <= c.grid_cap)
+        sweep_kernel<K, true, 4><<<grid, 32, size_t(Geom<K, 4>::TOTAL) * sizeof(float), s>>>(A);
+    else
+        sweep_kernel<K, true, kChunk><<<grid, 32, size_t(Geom<K, kChunk>::TOTAL) * sizeof(float), s>>>(A);
     return cudaGetLastError();
 }
 
-template <int K>
-cudaError_t launch_sweep_k(const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
-                           float eps, float omega, cudaStream_t s) {
-    static int grid_cap = 0;
-    if (grid_cap == 0) {
-        constexpr size_t smem = size_t(Geom<K, kChunk>::TOTAL) * sizeof(float);
-        cudaError_t e = cudaFuncSetAttribute(sweep_kernel<K, true, kChunk>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(sweep_kernel<K, true, kChunk>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e != cudaSuccess) return e;
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<K, true, kChunk>, 32, smem);
-        if (const char* e = std::getenv("FGM_SWEEP_WARPS_PER_SM")) per_sm = std::min(per_sm, std::atoi(e));  // tuning
-        grid_cap = std::max(1, sms * std::max(1, per_sm));
-    }
-    static int waves = -1;
-    if (waves < 0) {
-        const char* e = std::getenv("FGM_CHUNK4_WAVES");  // tuning knob
-        waves = e ? std::atoi(e) : 1;
-    }
-#ifndef FGM_LAT_CHUNK
-#define FGM_LAT_CHUNK 4
-#endif
-    if (total_items <= waves * grid_cap)
-        return launch_sweep_kc<K, FGM_LAT_CHUNK>(jobs_dev, order_dev, total_items, ticket, eps, omega, s, grid_cap);
-    return launch_sweep_kc<K, kChunk>(jobs_dev, order_dev, total_items, ticket, eps, omega, s, grid_cap);
-}
-
-__global__ void stream_fill_kernel(const SweepJob* __restrict__ jobs, int K, bool full) {
+__global__ void stream_fill_kernel(const SweepJob* __restrict__ jobs, int K) {
     const SweepJob J = jobs[blockIdx.y];
-    const size_t n = size_t(J.nb) * (full ? sweep_full_stream_len(J.w, K) : 3 * sweep_stream_len(J.w, K)) / 4;
+    const size_t n = size_t(J.nb) * 3 * sweep_stream_len(J.w, K) / 4;
     float4* p = reinterpret_cast<float4*>(J.stream);
     const float s = __uint_as_float(kStreamSentinel);
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
@@ -900,11 +957,10 @@ __global__ void stream_fill_kernel(const SweepJob* __restrict__ jobs, int K, boo
 
 }  // namespace
 
-cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, bool full, size_t max_floats,
-                               cudaStream_t s) {
+cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, size_t max_floats, cudaStream_t s) {
     if (njobs <= 0) return cudaSuccess;
     const int gx = int(std::min<size_t>(std::max<size_t>((max_floats / 4 + 255) / 256, 1), 64));
-    stream_fill_kernel<<<dim3(gx, njobs), 256, 0, s>>>(jobs_dev, K, full);
+    stream_fill_kernel<<<dim3(gx, njobs), 256, 0, s>>>(jobs_dev, K);
     return cudaGetLastError();
 }
 
@@ -926,13 +982,27 @@ size_t sweep_smem_bytes(int K) {
     }
 }
 
+std::atomic<int> g_sweep_fault{0};
+std::atomic<long long> g_spin_timeout_ns{2000000000ll};
+
 cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
-                         float eps, float omega, cudaStream_t s) {
+                         float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s) {
+    SweepArgs A;
+    A.jobs = jobs_dev;
+    A.order = order_dev;
+    A.total = total_items;
+    A.ticket = ticket;
+    A.eps = eps;
+    A.omega = omega;
+    A.fail.abort_flag = abort_flag;
+    A.fail.fault_count = fault_count;
+    A.fail.spin_ns = (unsigned long long)std::max<long long>(g_spin_timeout_ns.load(), 1000);
+    A.fault = g_sweep_fault.load();
     switch (K) {
-        case 1: return launch_sweep_k<1>(jobs_dev, order_dev, total_items, ticket, eps, omega, s);
-        case 2: return launch_sweep_k<2>(jobs_dev, order_dev, total_items, ticket, eps, omega, s);
-        case 3: return launch_sweep_k<3>(jobs_dev, order_dev, total_items, ticket, eps, omega, s);
-        case 4: return launch_sweep_k<4>(jobs_dev, order_dev, total_items, ticket, eps, omega, s);
+        case 1: return launch_sweep_k<1>(A, s);
+        case 2: return launch_sweep_k<2>(A, s);
+        case 3: return launch_sweep_k<3>(A, s);
+        case 4: return launch_sweep_k<4>(A, s);
         default: return cudaErrorInvalidValue;
     }
 }

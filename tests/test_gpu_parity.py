@@ -403,53 +403,6 @@ def test_fused_pyramid_bitwise(fgm, cuda):
             assert torch.equal(lx, ly)
 
 
-@pytest.mark.parametrize("kw", [dict(), dict(iters_high=1), dict(iters_high=3), dict(iters_high=5)])
-def test_sweep_kernels_agree_bitwise(fgm, cuda, oracle_mod, kw):
-    # the two experimental K3 variants (full-channel warps with passed
-    # coefficients; band CTAs with a coefficient warp) run the same A/A2/Bc
-    # arithmetic, so the same bits; the default kernel (rank-one form) agrees
-    # with them within the oracle tolerance
-    from paper_2006_14970_b200 import synth
-
-    p = params_from(fgm, oracle_mod.Params(**kw))
-    imgs, alps = [], []
-    for i, (w, h) in enumerate([(700, 300), (257, 513), (96, 64), (1000, 33)]):
-        im, al = synth.make_composite(w, h, 300 + i, 4, 3.0)
-        imgs.append(im.to(cuda))
-        alps.append(al.to(cuda))
-    try:
-        fgm.set_sweep_mode(1)
-        a = fgm.batch_solve_cuda(imgs, alps, p)
-        fgm.set_sweep_mode(2)
-        b = fgm.batch_solve_cuda(imgs, alps, p)
-        fgm.set_sweep_mode(3)  # band CTAs with a shared coefficient warp
-        c = fgm.batch_solve_cuda(imgs, alps, p)
-    finally:
-        fgm.set_sweep_mode(0)
-    # (the band-CTA kernel exists for K <= 2; K = 3 passes fall back to the default kernel)
-    cta_everywhere = kw.get("iters_high", 2) in (1, 2)
-    for (fa, ba), (fb, bb), (fc, bc) in zip(a, b, c):
-        if cta_everywhere:
-            assert torch.equal(fb, fc) and torch.equal(bb, bc)
-        for x, y in ((fa, fb), (ba, bb), (fa, fc), (ba, bc)):
-            assert (x - y).abs().max().item() <= TOL_MAX
-
-
-def test_full_channel_kernel_vs_oracle(fgm, cuda, orc, oracle_mod):
-    from paper_2006_14970_b200 import synth
-
-    img, a = synth.make_composite(333, 517, 17, 4, 3.0)
-    try:
-        fgm.set_sweep_mode(2)
-        for p in (oracle_mod.Params(), oracle_mod.REFERENCE_DEFAULTS, oracle_mod.Params(iters_high=3)):
-            f, b = gpu_solve(fgm, cuda, img.numpy(), a.numpy(), p)
-            of, ob = orc.ml_solve(img.double().numpy(), a.double().numpy(), p)
-            assert_close("fg", f, of)
-            assert_close("bg", b, ob)
-    finally:
-        fgm.set_sweep_mode(0)
-
-
 # ---- reentrancy: concurrent solves from several host threads ----
 def test_concurrent_host_threads(fgm, cuda):
     import threading
@@ -576,3 +529,32 @@ def test_random_sizes_and_params_vs_oracle(fgm, cuda, orc, oracle_mod, seed):
         assert_close("bg", b.double().cpu().numpy(), ob)
         f1, b1 = gpu_solve(fgm, cuda, im.numpy(), al.numpy(), p)
         assert np.array_equal(f1, f.double().cpu().numpy()) and np.array_equal(b1, b.double().cpu().numpy())
+
+
+# ---- failure detection: a stalled band hand-over is an error, not a hang ----
+@pytest.mark.gpu
+def test_stalled_handover_returns_runtime_error(fgm, cuda):
+    """SURVEY.md section 5 ("timeout -> error, not a hang"): with band 0 of every
+    sweep made to skip publishing its boundary stream (fgm_debug_fault(1)), band
+    1 waits for data that never comes; the bounded wait aborts the launch, counts
+    a device fault and the synchronous entry point returns FGM_RUNTIME_ERROR."""
+    from paper_2006_14970_b200 import synth
+
+    img, a = synth.make_composite(300, 200, 4242, 4, 3.0)  # 7 bands at the top level
+    fgm.device_faults(reset=True)
+    fgm.set_spin_timeout_ms(100)
+    fgm.debug_fault(1)
+    try:
+        with pytest.raises(RuntimeError, match="timed out"):
+            fgm.ml_foreground_background(img.permute(1, 2, 0).double().numpy(), a.double().numpy(),
+                                         **fgm.BASELINE_PARAMS.kwargs())
+        assert fgm.device_faults() > 0
+    finally:
+        fgm.debug_fault(0)
+        fgm.set_spin_timeout_ms(2000)
+        fgm.device_faults(reset=True)
+    # the device and the library stay usable
+    f, b = fgm.ml_foreground_background(img.permute(1, 2, 0).double().numpy(), a.double().numpy(),
+                                        **fgm.BASELINE_PARAMS.kwargs())
+    assert np.isfinite(f).all() and np.isfinite(b).all()
+    assert fgm.device_faults() == 0

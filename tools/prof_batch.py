@@ -1,5 +1,5 @@
 """Warm-up + one batch solve of config 4 (for ncu capture of the sweep kernel).
-Usage: prof_batch.py [n_images] [sweep_mode]"""
+Usage: prof_batch.py [n_images]"""
 import sys
 
 import torch
@@ -9,8 +9,6 @@ import paper_2006_14970_b200 as fgm  # noqa: E402
 from paper_2006_14970_b200 import synth  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-if len(sys.argv) > 2:
-    fgm.set_sweep_mode(int(sys.argv[2]))
 batch = synth.make_batch(n, device="cuda")
 imgs = [b[0] for b in batch]
 alps = [b[1] for b in batch]

@@ -9,10 +9,7 @@ import paper_2006_14970_b200 as fgm  # noqa: E402
 from paper_2006_14970_b200 import synth  # noqa: E402
 
 dev = torch.device("cuda:0")
-which = [a for a in sys.argv[1:] if not a.startswith("mode=")] or ["1", "2", "3", "5"]
-for a in sys.argv[1:]:
-    if a.startswith("mode="):
-        fgm.set_sweep_mode(int(a[5:]))
+which = sys.argv[1:] or ["1", "2", "3", "5"]
 cfgs = {"1": synth.C1, "2": synth.C2, "3": synth.C3, "5": synth.C5}
 for c in which:
     cfg = cfgs[c]
