@@ -71,3 +71,23 @@ def test_gloo_world2_sharding():
     assert res[0][2] == res[1][2] == 13.0  # max over ranks
     assert res[0][3] == sum(w * h for w, h in sizes)
     assert shards0 == shard.lpt_partition(sizes, 2)
+
+
+def test_bench_rank_and_shard_path_world2():
+    """bench.py's multi-GPU path end to end on CPU: `--gpus 2` re-launches
+    itself under torch.distributed.run (127.0.0.1), both ranks take their LPT
+    shards over gloo, the shards partition the 256-image batch, the timing
+    goes through max-over-ranks, and rank 0's line reports n_gpus = 2."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--cpu-dry-run"],
+                         capture_output=True, text=True, timeout=240, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["partition_ok"] and sum(d["shards"]) == 256
+    assert abs(d["megapixels"] - d["config"]["megapixels"]) < 1e-3  # (config rounds to 3 decimals)

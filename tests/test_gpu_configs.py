@@ -2,16 +2,16 @@
 8(d)), at BASELINE params: regularization=1e-5, gradient_weight=1.0, 10 small
 / 2 big iterations (8 for config 5), small_size=32.
 
-C1-C3 and a sample of C4 are compared with the fp64 oracle at full size.  C5
-(16384^2, k=8) is too large for the oracle in a test (~45 GB, minutes), so it
-is checked through size-independent properties at full size (range,
-determinism, exchange symmetry, binary-alpha recovery) and through oracle
-parity of the same generator at 2048^2 with k=8."""
+C1-C3, C5 (16384^2, k=8; ~2.5 minutes and ~60 GB of host memory for the fp64
+oracle) and a sample of C4 are compared with the fp64 oracle at full size; C5
+is also checked through size-independent properties at full size (range,
+determinism, exchange symmetry, reconstruction).  The full 256-image C4 batch
+is compared with the reference by bench.py (its `parity` block)."""
 import numpy as np
 import pytest
 import torch
 
-from conftest import assert_close
+from conftest import TOL_MAX, TOL_MEAN, assert_close
 
 pytestmark = pytest.mark.gpu
 
@@ -70,6 +70,35 @@ def test_c5_generator_k8_at_2048_vs_oracle(fgm, cuda, orc, oracle_mod):
     of, ob = orc.ml_solve(img.double().numpy(), a.double().numpy(), oracle_params(oracle_mod, 8))
     assert_close("fg", f.double().cpu().numpy(), of)
     assert_close("bg", b.double().cpu().numpy(), ob)
+
+
+def test_c5_full_size_vs_oracle(fgm, cuda, orc, oracle_mod):
+    """BASELINE configs[4] at full size against the fp64 oracle (bitwise equal to
+    the reference, tests/test_oracle.py): the only config whose top level runs
+    the K = 4, 16-column-chunk sweep (sweep_kernel<4, true, 16>)."""
+    from paper_2006_14970_b200 import synth
+
+    img, a = synth.make_config(synth.C5, device="cuda")
+    f, b = fgm.ml_foreground_background_cuda(img, a, fparams(fgm, 8))
+    torch.cuda.synchronize()
+    fh, bh = f.cpu().numpy(), b.cpu().numpy()
+    del f, b
+    imh, ah = img.cpu().numpy(), a.cpu().numpy()
+    del img, a
+    torch.cuda.empty_cache()
+    of, ob = orc.ml_solve(imh, ah, oracle_params(oracle_mod, 8))
+    del imh, ah
+    worst, total, n = 0.0, 0.0, 0
+    for got, want in ((fh, of), (bh, ob)):
+        for c in range(3):
+            for r0 in range(0, got.shape[1], 2048):  # bounded temporaries
+                d = np.abs(got[c, r0:r0 + 2048].astype(np.float64) - want[c, r0:r0 + 2048])
+                worst = max(worst, float(d.max()))
+                total += float(d.sum())
+                n += d.size
+    mean = total / n
+    print(f"C5 16384^2 k=8 vs oracle: max {worst:.3g} mean {mean:.3g}")
+    assert worst <= TOL_MAX and mean <= TOL_MEAN, f"C5: max {worst:.3g} mean {mean:.3g}"
 
 
 def test_c5_full_size_properties(fgm, cuda):

@@ -558,3 +558,28 @@ def test_stalled_handover_returns_runtime_error(fgm, cuda):
                                         **fgm.BASELINE_PARAMS.kwargs())
     assert np.isfinite(f).all() and np.isfinite(b).all()
     assert fgm.device_faults() == 0
+
+
+# ---- the K = 4 throughput sweep (16-column chunks) against the oracle -------
+@pytest.mark.gpu
+def test_k4_throughput_launch_vs_oracle(fgm, cuda, orc, oracle_mod):
+    """iters_high = 4 fuses the two big-level sweeps of every big level into one
+    K = 4 pass; 16 images of 1024^2 give 16 x 33 bands x 3 channels = 1584
+    (band, channel) items in the top-level launch, more than the GPU holds at
+    once (148 SMs x 8 warps), so it runs the throughput instantiation
+    (sweep_kernel<4, true, 16>) that config 5 uses at its top level."""
+    from paper_2006_14970_b200 import synth
+
+    n = 16
+    imgs, alps = [], []
+    for i in range(n):
+        im, al = synth.make_composite(1024, 1024, 7100 + i, 6, 4.0)
+        imgs.append(im)
+        alps.append(al)
+    p = oracle_mod.Params(omega=1.0, eps_r=1e-5, low_res_threshold=32, iters_low=10, iters_high=4)
+    outs = fgm.batch_solve_cuda([x.to(cuda) for x in imgs], [x.to(cuda) for x in alps], params_from(fgm, p))
+    torch.cuda.synchronize()
+    for i in (0, n - 1):
+        of, ob = orc.ml_solve(imgs[i].double().numpy(), alps[i].double().numpy(), p)
+        assert_close(f"K4 batch fg {i}", outs[i][0].double().cpu().numpy(), of)
+        assert_close(f"K4 batch bg {i}", outs[i][1].double().cpu().numpy(), ob)
