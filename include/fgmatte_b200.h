@@ -175,6 +175,12 @@ int fgm_kernel_stats(int which, long long* launches, double* ms, double* alg_byt
  * Writes at most `max` entries; returns the number of launches. */
 int fgm_profile_timeline(int max, int* which, double* t0, double* t1);
 
+/* Workspace comes from the library's own stream-ordered memory pool on each
+ * device, kept mapped between calls (the process's default pool is not
+ * touched).  fgm_release_memory() synchronises the current device and returns
+ * that pool's unused memory to the system. */
+int fgm_release_memory(void);
+
 const char* fgm_last_error(void);
 int fgm_device_count(void);
 const char* fgm_version(void);

@@ -169,6 +169,11 @@ def device_faults(reset: bool = False) -> int:
     return n
 
 
+def release_memory() -> None:
+    """Return the library's cached workspace on the current device (fgm_release_memory)."""
+    _check(_load().fgm_release_memory())
+
+
 def version() -> str:
     return _load().fgm_version().decode()
 
@@ -282,8 +287,9 @@ def _ml_foreground_background_hwc_device(image, alpha, params):
     fg = torch.empty((h, w, 3), device=image.device, dtype=dt)
     bg = torch.empty_like(fg)
     p = params.c()
-    _check(_load().fgm_ml_solve_hwc(image.data_ptr(), alpha.data_ptr(), w, h, 1 if dt == torch.float64 else 0,
-                                    C.byref(p), fg.data_ptr(), bg.data_ptr(), _stream_ptr(image.device)))
+    with _on(image.device):
+        _check(_load().fgm_ml_solve_hwc(image.data_ptr(), alpha.data_ptr(), w, h, 1 if dt == torch.float64 else 0,
+                                        C.byref(p), fg.data_ptr(), bg.data_ptr(), _stream_ptr(image.device)))
     return fg, bg
 
 
@@ -310,12 +316,34 @@ def _stream_ptr(dev) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 
 
-def _dev_f32(t, name):
+def _dev_f32(t, name, device=None):
     import torch
 
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
         raise TypeError(f"{name} must be a float32 CUDA tensor")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device} (all tensors of a call on one device)")
     return t.contiguous()
+
+
+def _on(device):
+    """Make `device` current for the C ABI call (it runs on cudaGetDevice())."""
+    import torch
+
+    return torch.cuda.device(device)
+
+
+def _check_out(t, shape, device, name):
+    """A caller-supplied output: written through its data pointer by the C ABI,
+    so it must be exactly a contiguous float32 tensor of the right shape and
+    device (host when device is None)."""
+    import torch
+
+    ok = isinstance(t, torch.Tensor) and t.dtype == torch.float32 and t.is_contiguous() and tuple(t.shape) == shape
+    ok = ok and ((not t.is_cuda) if device is None else (t.is_cuda and t.device == device))
+    if not ok:
+        where = "host" if device is None else str(device)
+        raise ValueError(f"{name} must be a contiguous float32 tensor of shape {shape} on {where}")
 
 
 def ml_foreground_background_cuda(image, alpha, params: Params = Params()):
@@ -324,19 +352,25 @@ def ml_foreground_background_cuda(image, alpha, params: Params = Params()):
     import torch
 
     image = _dev_f32(image, "image")
-    alpha = _dev_f32(alpha, "alpha")
-    if image.dim() != 3 or image.shape[0] != 3:
-        raise ValueError(f"ml_foreground_background: image must have 3 channels, got shape {tuple(image.shape)}")
+    alpha = _dev_f32(alpha, "alpha", image.device)
+    _check_image_alpha(image, alpha)
     h, w = image.shape[1], image.shape[2]
-    if tuple(alpha.shape) != (h, w):
-        raise ValueError(f"ml_foreground_background: alpha size {alpha.shape[-1]}x{alpha.shape[0]} does not match "
-                         f"image size {w}x{h}")
     fg = torch.empty_like(image)
     bg = torch.empty_like(image)
     p = params.c()
-    _check(_load().fgm_ml_solve_f32(image.data_ptr(), alpha.data_ptr(), w, h, C.byref(p), fg.data_ptr(),
-                                    bg.data_ptr(), _stream_ptr(image.device)))
+    with _on(image.device):
+        _check(_load().fgm_ml_solve_f32(image.data_ptr(), alpha.data_ptr(), w, h, C.byref(p), fg.data_ptr(),
+                                        bg.data_ptr(), _stream_ptr(image.device)))
     return fg, bg
+
+
+def _check_image_alpha(image, alpha):
+    if image.dim() != 3 or image.shape[0] != 3:
+        raise ValueError(f"ml_foreground_background: image must have 3 channels, got shape {tuple(image.shape)}")
+    h, w = image.shape[1], image.shape[2]
+    if alpha.dim() != 2 or tuple(alpha.shape) != (h, w):
+        raise ValueError(f"ml_foreground_background: alpha size {tuple(alpha.shape)} does not match image size "
+                         f"{w}x{h}")
 
 
 def ml_foreground_background_levels_cuda(image, alpha, params: Params = Params()):
@@ -344,7 +378,8 @@ def ml_foreground_background_levels_cuda(image, alpha, params: Params = Params()
     import torch
 
     image = _dev_f32(image, "image")
-    alpha = _dev_f32(alpha, "alpha")
+    alpha = _dev_f32(alpha, "alpha", image.device)
+    _check_image_alpha(image, alpha)
     h, w = image.shape[1], image.shape[2]
     sched = level_schedule(w, h, params.omega, params.eps_r, params.low_res_threshold, params.iters_low,
                            params.iters_high)
@@ -356,8 +391,9 @@ def ml_foreground_background_levels_cuda(image, alpha, params: Params = Params()
     fa = (C.c_void_p * n)(*[x.data_ptr() for x in lf])
     ba = (C.c_void_p * n)(*[x.data_ptr() for x in lb])
     p = params.c()
-    _check(_load().fgm_ml_solve_levels_f32(image.data_ptr(), alpha.data_ptr(), w, h, C.byref(p), fg.data_ptr(),
-                                           bg.data_ptr(), fa, ba, n, _stream_ptr(image.device)))
+    with _on(image.device):
+        _check(_load().fgm_ml_solve_levels_f32(image.data_ptr(), alpha.data_ptr(), w, h, C.byref(p), fg.data_ptr(),
+                                               bg.data_ptr(), fa, ba, n, _stream_ptr(image.device)))
     return fg, bg, lf, lb
 
 
@@ -370,22 +406,28 @@ def batch_solve_cuda(images: Sequence, alphas: Sequence, params: Params = Params
     n = len(images)
     if len(alphas) != n:
         raise ValueError("batch_solve_cuda: images and alphas differ in length")
-    imgs = [_dev_f32(x, "image") for x in images]
-    alps = [_dev_f32(x, "alpha") for x in alphas]
+    if n == 0:
+        return [] if outputs is None else outputs
+    dev = images[0].device if isinstance(images[0], torch.Tensor) else None
+    imgs = [_dev_f32(x, "image", dev) for x in images]
+    alps = [_dev_f32(x, "alpha", dev) for x in alphas]
+    for x, a in zip(imgs, alps):
+        _check_image_alpha(x, a)
     if outputs is None:
         outputs = [(torch.empty_like(x), torch.empty_like(x)) for x in imgs]
-    if n == 0:
-        return outputs
-    for x, a in zip(imgs, alps):
-        if x.dim() != 3 or x.shape[0] != 3 or tuple(a.shape) != tuple(x.shape[1:]):
-            raise ValueError("batch_solve_cuda: bad image/alpha shapes")
+    if len(outputs) != n:
+        raise ValueError("batch_solve_cuda: outputs and images differ in length")
+    for x, (f, b) in zip(imgs, outputs):
+        _check_out(f, tuple(x.shape), dev, "batch_solve_cuda output fg")
+        _check_out(b, tuple(x.shape), dev, "batch_solve_cuda output bg")
     V = C.c_void_p * n
     ws = (C.c_int * n)(*[x.shape[2] for x in imgs])
     hs = (C.c_int * n)(*[x.shape[1] for x in imgs])
     p = params.c()
-    _check(_load().fgm_batch_solve_f32(n, V(*[x.data_ptr() for x in imgs]), V(*[a.data_ptr() for a in alps]), ws,
-                                       hs, C.byref(p), V(*[o[0].data_ptr() for o in outputs]),
-                                       V(*[o[1].data_ptr() for o in outputs]), _stream_ptr(imgs[0].device)))
+    with _on(dev):
+        _check(_load().fgm_batch_solve_f32(n, V(*[x.data_ptr() for x in imgs]), V(*[a.data_ptr() for a in alps]),
+                                           ws, hs, C.byref(p), V(*[o[0].data_ptr() for o in outputs]),
+                                           V(*[o[1].data_ptr() for o in outputs]), _stream_ptr(dev)))
     return outputs
 
 
@@ -403,10 +445,17 @@ def batch_solve_host(images: Sequence, alphas: Sequence, params: Params = Params
             raise TypeError("batch_solve_host: images must be contiguous host float32 (3, H, W)")
         if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous() or tuple(a.shape) != tuple(x.shape[1:]):
             raise TypeError("batch_solve_host: alphas must be contiguous host float32 (H, W)")
+    if len(alps) != n:
+        raise ValueError("batch_solve_host: images and alphas differ in length")
     if outputs is None:
         outputs = [(torch.empty_like(x), torch.empty_like(x)) for x in imgs]
     if n == 0:
         return outputs
+    if len(outputs) != n:
+        raise ValueError("batch_solve_host: outputs and images differ in length")
+    for x, (f, b) in zip(imgs, outputs):
+        _check_out(f, tuple(x.shape), None, "batch_solve_host output fg")
+        _check_out(b, tuple(x.shape), None, "batch_solve_host output bg")
     V = C.c_void_p * n
     ws = (C.c_int * n)(*[x.shape[2] for x in imgs])
     hs = (C.c_int * n)(*[x.shape[1] for x in imgs])
@@ -427,8 +476,9 @@ def resize_cuda(src, width: int, height: int):
     if width < 1 or height < 1:
         raise ValueError(f"resize: target size must be >= 1x1, got {width}x{height}")
     out = torch.empty((src.shape[0], height, width), device=src.device, dtype=torch.float32)
-    _check(_load().fgm_resize_f32(src.data_ptr(), src.shape[2], src.shape[1], src.shape[0], out.data_ptr(), width,
-                                  height, _stream_ptr(src.device)))
+    with _on(src.device):
+        _check(_load().fgm_resize_f32(src.data_ptr(), src.shape[2], src.shape[1], src.shape[0], out.data_ptr(),
+                                      width, height, _stream_ptr(src.device)))
     return out
 
 
@@ -442,8 +492,9 @@ def evaluate_metrics_cuda(est, gt, alpha, sigma: float = 1.4, kernel_radius: int
     if tuple(alpha.shape) != tuple(est.shape[1:]):
         raise ValueError(f"sad: alpha size {tuple(alpha.shape)} does not match images {tuple(est.shape[1:])}")
     out = (C.c_double * 4)()
-    _check(_load().fgm_metrics_f32(est.data_ptr(), gt.data_ptr(), alpha.data_ptr(), est.shape[2], est.shape[1],
-                                   est.shape[0], float(sigma), int(kernel_radius), out, _stream_ptr(est.device)))
+    with _on(est.device):
+        _check(_load().fgm_metrics_f32(est.data_ptr(), gt.data_ptr(), alpha.data_ptr(), est.shape[2], est.shape[1],
+                                       est.shape[0], float(sigma), int(kernel_radius), out, _stream_ptr(est.device)))
     return {"sad": out[0], "mse": out[1], "grad": out[2], "translucent_pixel_count": int(out[3])}
 
 
@@ -459,9 +510,13 @@ def compose_cuda(fg, bg, alpha, out=None):
         raise ValueError(f"compose: bg size {tuple(bg.shape)} does not match fg size {tuple(fg.shape)}")
     if tuple(alpha.shape) != tuple(fg.shape[1:]):
         raise ValueError(f"compose: alpha size {tuple(alpha.shape)} does not match fg size {tuple(fg.shape[1:])}")
-    out = torch.empty_like(fg) if out is None else out
-    _check(_load().fgm_compose_f32(fg.data_ptr(), bg.data_ptr(), alpha.data_ptr(), fg.shape[2], fg.shape[1],
-                                   fg.shape[0], out.data_ptr(), _stream_ptr(fg.device)))
+    if out is None:
+        out = torch.empty_like(fg)
+    else:
+        _check_out(out, tuple(fg.shape), fg.device, "compose output")
+    with _on(fg.device):
+        _check(_load().fgm_compose_f32(fg.data_ptr(), bg.data_ptr(), alpha.data_ptr(), fg.shape[2], fg.shape[1],
+                                       fg.shape[0], out.data_ptr(), _stream_ptr(fg.device)))
     return out
 
 
@@ -469,13 +524,17 @@ def sweep_passes_cuda(image, alpha, fg, bg, iterations: int, eps_r: float, omega
     """`iterations` exact Gauss-Seidel sweeps of one level (multilevel.cpp:81-121)."""
     import torch
 
-    image, alpha = _dev_f32(image, "image"), _dev_f32(alpha, "alpha")
-    fg, bg = _dev_f32(fg, "fg"), _dev_f32(bg, "bg")
+    image = _dev_f32(image, "image")
+    alpha, fg, bg = (_dev_f32(t, n, image.device) for t, n in ((alpha, "alpha"), (fg, "fg"), (bg, "bg")))
+    _check_image_alpha(image, alpha)
+    if tuple(fg.shape) != tuple(image.shape) or tuple(bg.shape) != tuple(image.shape):
+        raise ValueError(f"sweep_passes: fg/bg must have the image's shape {tuple(image.shape)}")
     h, w = image.shape[1], image.shape[2]
     fo, bo = torch.empty_like(fg), torch.empty_like(bg)
-    _check(_load().fgm_sweep_passes_f32(image.data_ptr(), alpha.data_ptr(), fg.data_ptr(), bg.data_ptr(), w, h,
-                                        int(iterations), float(eps_r), float(omega), fo.data_ptr(), bo.data_ptr(),
-                                        _stream_ptr(image.device)))
+    with _on(image.device):
+        _check(_load().fgm_sweep_passes_f32(image.data_ptr(), alpha.data_ptr(), fg.data_ptr(), bg.data_ptr(), w, h,
+                                            int(iterations), float(eps_r), float(omega), fo.data_ptr(),
+                                            bo.data_ptr(), _stream_ptr(image.device)))
     return fo, bo
 
 

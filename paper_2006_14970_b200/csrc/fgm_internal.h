@@ -5,8 +5,37 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 
 namespace fgm {
+
+// A lazily initialised value per CUDA device (function attributes, occupancy,
+// memory pools are per device; a process may drive several GPUs from several
+// host threads).  init(dev, value&) runs once per device under a lock.
+template <class T>
+class PerDevice {
+   public:
+    template <class F>
+    cudaError_t get(T& out, F&& init) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (dev < 0 || dev >= kMax) return cudaErrorInvalidDevice;
+        std::lock_guard<std::mutex> g(mu_);
+        if (!ok_[dev]) {
+            if ((e = init(dev, v_[dev])) != cudaSuccess) return e;
+            ok_[dev] = true;
+        }
+        out = v_[dev];
+        return cudaSuccess;
+    }
+
+   private:
+    static constexpr int kMax = 64;
+    std::mutex mu_;
+    T v_[kMax]{};
+    bool ok_[kMax] = {};
+};
 
 // ---- K1/K2: bilinear resample (image.cpp:71-133) --------------------------
 struct ResampleJob {

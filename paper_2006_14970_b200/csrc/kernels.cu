@@ -308,17 +308,17 @@ int upsample_tiles(int dw, int dh) { return ((dw + kUpCols - 1) / kUpCols) * ((d
 cudaError_t launch_upsample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s) {
     if (njobs <= 0 || total_tiles <= 0) return cudaSuccess;
     constexpr size_t smem = size_t(2) * kUpBuf * sizeof(float);
-    static int per_sm = 0, sms = 0;
-    if (!per_sm) {
-        cudaError_t e = cudaFuncSetAttribute(upsample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upsample_kernel, kUpThreads, smem);
-        per_sm = std::max(per_sm, 1);
-    }
-    const int gx = int(std::min<long long>(total_tiles, (long long)sms * per_sm));
+    static PerDevice<int2> cfg;  // (SMs, blocks per SM)
+    int2 c;
+    cudaError_t e = cfg.get(c, [&](int dev, int2& v) {
+        cudaError_t r = cudaFuncSetAttribute(upsample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (r == cudaSuccess) r = cudaDeviceGetAttribute(&v.x, cudaDevAttrMultiProcessorCount, dev);
+        if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v.y, upsample_kernel, kUpThreads, smem);
+        v.y = std::max(v.y, 1);
+        return r;
+    });
+    if (e != cudaSuccess) return e;
+    const int gx = int(std::min<long long>(total_tiles, (long long)c.x * c.y));
     upsample_kernel<<<gx, kUpThreads, smem, s>>>(jobs_dev, njobs, int(total_tiles));
     return cudaGetLastError();
 }
@@ -333,12 +333,10 @@ int resample_tiles(int dw, int dh) { return ((dw + kResCols - 1) / kResCols) * (
 cudaError_t launch_resample(const ResampleJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s,
                             int blocks_per_sm) {
     if (njobs <= 0 || total_tiles <= 0) return cudaSuccess;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    static PerDevice<int> cfg;  // SMs
+    int sms = 0;
+    cudaError_t e = cfg.get(sms, [](int dev, int& v) { return cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev); });
+    if (e != cudaSuccess) return e;
     // blocks_per_sm 0: one tile per block (no persistent blocks holding SM slots)
     const int gx = int(blocks_per_sm > 0 ? std::min<long long>(total_tiles, (long long)sms * blocks_per_sm) : total_tiles);
     resample_kernel<<<gx, kResCols, 0, s>>>(jobs_dev, njobs, int(total_tiles));
@@ -509,17 +507,17 @@ __global__ void __launch_bounds__(kPyrThreads) pyramid_kernel(const PyrJob* __re
 cudaError_t launch_pyramid(const PyrJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s) {
     if (njobs <= 0 || total_tiles <= 0) return cudaSuccess;
     constexpr size_t smem = size_t(2) * kPyrBuf * sizeof(float);
-    static int per_sm = 0, sms = 0;
-    if (!per_sm) {
-        cudaError_t e = cudaFuncSetAttribute(pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pyramid_kernel, kPyrThreads, smem);
-        per_sm = std::max(per_sm, 1);
-    }
-    const int gx = int(std::min<long long>(total_tiles, (long long)sms * per_sm));
+    static PerDevice<int2> cfg;  // (SMs, blocks per SM)
+    int2 c;
+    cudaError_t e = cfg.get(c, [&](int dev, int2& v) {
+        cudaError_t r = cudaFuncSetAttribute(pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (r == cudaSuccess) r = cudaDeviceGetAttribute(&v.x, cudaDevAttrMultiProcessorCount, dev);
+        if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v.y, pyramid_kernel, kPyrThreads, smem);
+        v.y = std::max(v.y, 1);
+        return r;
+    });
+    if (e != cudaSuccess) return e;
+    const int gx = int(std::min<long long>(total_tiles, (long long)c.x * c.y));
     pyramid_kernel<<<gx, kPyrThreads, smem, s>>>(jobs_dev, njobs, int(total_tiles));
     return cudaGetLastError();
 }
@@ -784,13 +782,12 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_kernel(const CoarseJob*
 
 cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float omega, cudaStream_t s) {
     if (njobs <= 0) return cudaSuccess;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(coarse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(coarse_smem_bytes()));
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static PerDevice<int> attr;  // the > 48 KB shared-memory opt-in, per device
+    int unused = 0;
+    cudaError_t e = attr.get(unused, [](int, int&) {
+        return cudaFuncSetAttribute(coarse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(coarse_smem_bytes()));
+    });
+    if (e != cudaSuccess) return e;
     coarse_kernel<<<njobs, kCoarseThreads, coarse_smem_bytes(), s>>>(jobs_dev, eps, omega);
     return cudaGetLastError();
 }

@@ -173,24 +173,41 @@ void prof_drain() {
     g_prof.clear();
 }
 
-// ---- device checks ---------------------------------------------------------
+// ---- device checks ----------------------------------------------------------
 void require_device() {
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
     if (e != cudaSuccess || n == 0)
         throw RuntimeError(std::string("no CUDA device available (") + cudaGetErrorString(e) +
                            "); fgmatte_b200 has no CPU fallback");
-    static bool pool_set = false;
-    if (!pool_set) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            unsigned long long thr = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        pool_set = true;
-    }
+}
+
+// The library's own stream-ordered memory pool on the current device.  Its
+// release threshold is unbounded: a solve's workspace (tens of GB for a large
+// batch) stays mapped for the next call instead of being unmapped and mapped
+// again at every synchronisation; fgm_release_memory() returns it.  The
+// process's default pool (used by other libraries) is left untouched.
+cudaMemPool_t device_pool() {
+    static PerDevice<cudaMemPool_t> pools;
+    cudaMemPool_t p = nullptr;
+    ck(pools.get(p, [](int dev, cudaMemPool_t& v) {
+           cudaMemPoolProps props{};
+           props.allocType = cudaMemAllocationTypePinned;
+           props.handleTypes = cudaMemHandleTypeNone;
+           props.location.type = cudaMemLocationTypeDevice;
+           props.location.id = dev;
+           cudaError_t e = cudaMemPoolCreate(&v, &props);
+           if (e != cudaSuccess) return e;
+           unsigned long long thr = ~0ull;
+           return cudaMemPoolSetAttribute(v, cudaMemPoolAttrReleaseThreshold, &thr);
+       }),
+       "cudaMemPoolCreate");
+    return p;
+}
+
+template <class T>
+void pool_alloc(T** p, size_t bytes, cudaStream_t s, const char* what) {
+    ck(cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, device_pool(), s), what);
 }
 
 ResampleJob rjob(const float* src, float* dst, int sw, int sh, int dw, int dh, int np, int spitch, int dpitch) {
@@ -240,7 +257,7 @@ struct Arena {
         s = st;
         guarded_ = g_debug_guards.load() != 0;
         size = bytes + (guarded_ ? max_takes * kGuardBytes : 0);
-        if (size) ck(cudaMallocAsync(reinterpret_cast<void**>(&base), size, s), "cudaMallocAsync");
+        if (size) pool_alloc(&base, size, s, "cudaMallocFromPoolAsync");
     }
     template <class T>
     T* take(size_t count) {
@@ -431,18 +448,14 @@ std::atomic<int> g_pyramid_mode{0};
 
 // Persistent per-device count of timed-out boundary-stream waits (sweep.cu).
 int* device_fault_counter() {
-    constexpr int kMaxDev = 64;
-    static std::mutex mu;
-    static int* ctr[kMaxDev] = {};
-    int dev = 0;
-    ck(cudaGetDevice(&dev), "cudaGetDevice");
-    if (dev < 0 || dev >= kMaxDev) throw RuntimeError("device index out of range");
-    std::lock_guard<std::mutex> g(mu);
-    if (!ctr[dev]) {
-        ck(cudaMalloc(reinterpret_cast<void**>(&ctr[dev]), sizeof(int)), "cudaMalloc(fault counter)");
-        ck(cudaMemset(ctr[dev], 0, sizeof(int)), "cudaMemset(fault counter)");
-    }
-    return ctr[dev];
+    static PerDevice<int*> ctr;
+    int* p = nullptr;
+    ck(ctr.get(p, [](int, int*& v) {
+           cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&v), sizeof(int));
+           return e == cudaSuccess ? cudaMemset(v, 0, sizeof(int)) : e;
+       }),
+       "cudaMalloc(fault counter)");
+    return p;
 }
 
 int read_faults() {
@@ -1069,16 +1082,32 @@ int fgm_batch_solve_host_f32(int n_images, const float* const* images, const flo
             gmax = std::max(gmax, px);
         }
         const size_t slot_floats = 10 * gmax + 64 * size_t(n_images);
-        float* dbuf = nullptr;
         const size_t nslots = std::min(kSlots, groups.size());
-        ck(cudaMallocAsync(reinterpret_cast<void**>(&dbuf), nslots * slot_floats * sizeof(float), sc),
-           "cudaMallocAsync");
-        std::vector<cudaEvent_t> ev_in(groups.size()), ev_done(groups.size()), ev_out(groups.size());
-        for (size_t g = 0; g < groups.size(); ++g) {
-            ck(cudaEventCreateWithFlags(&ev_in[g], cudaEventDisableTiming), "cudaEventCreate");
-            ck(cudaEventCreateWithFlags(&ev_done[g], cudaEventDisableTiming), "cudaEventCreate");
-            ck(cudaEventCreateWithFlags(&ev_out[g], cudaEventDisableTiming), "cudaEventCreate");
-        }
+        // owned resources, released on every exit (an exception included): the
+        // slots once all three streams are idle, then the events
+        struct Owned {
+            float* dbuf = nullptr;
+            std::vector<cudaEvent_t> ev;
+            cudaStream_t a, b, c;
+            ~Owned() {
+                if (dbuf) {
+                    cudaStreamSynchronize(a);
+                    cudaStreamSynchronize(b);
+                    cudaStreamSynchronize(c);
+                    cudaFreeAsync(dbuf, c);
+                    cudaStreamSynchronize(c);
+                }
+                for (cudaEvent_t e : ev)
+                    if (e) cudaEventDestroy(e);
+            }
+        } own{nullptr, {}, sin, sout, sc};
+        pool_alloc(&own.dbuf, nslots * slot_floats * sizeof(float), sc, "cudaMallocFromPoolAsync");
+        float* const dbuf = own.dbuf;
+        own.ev.assign(3 * groups.size(), nullptr);
+        for (cudaEvent_t& e : own.ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        cudaEvent_t* const ev_in = own.ev.data();
+        cudaEvent_t* const ev_done = ev_in + groups.size();
+        cudaEvent_t* const ev_out = ev_done + groups.size();
         ck(cudaStreamSynchronize(sc), "cudaStreamSynchronize");
         for (size_t g = 0; g < groups.size(); ++g) {
             const auto [b, e] = groups[g];
@@ -1112,13 +1141,7 @@ int fgm_batch_solve_host_f32(int n_images, const float* const* images, const flo
             ck(cudaEventRecord(ev_out[g], sout), "cudaEventRecord");
         }
         ck(cudaStreamSynchronize(sout), "cudaStreamSynchronize");
-        ck(cudaFreeAsync(dbuf, sc), "cudaFreeAsync");
         ck(cudaStreamSynchronize(sc), "cudaStreamSynchronize");
-        for (size_t g = 0; g < groups.size(); ++g) {
-            cudaEventDestroy(ev_in[g]);
-            cudaEventDestroy(ev_done[g]);
-            cudaEventDestroy(ev_out[g]);
-        }
         check_faults(faults0);
     });
 }
@@ -1342,6 +1365,14 @@ int fgm_profile_timeline(int max, int* which, double* t0, double* t1) {
         if (t1) t1[i] = g_timeline[size_t(i)].t1;
     }
     return n;
+}
+
+int fgm_release_memory(void) {
+    return guarded([&] {
+        require_device();
+        ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+        ck(cudaMemPoolTrimTo(device_pool(), 0), "cudaMemPoolTrimTo");
+    });
 }
 
 const char* fgm_last_error(void) { return fgm::g_err.c_str(); }

@@ -881,52 +881,28 @@ __global__ void __launch_bounds__(32, 1) sweep_kernel(SweepArgs A) {
     }
 }
 
-// Per-device launch state: the function attributes and the resident-warp
-// capacity are per device (a process may drive several GPUs from several
-// host threads).
-struct SweepCfg {
-    int grid_cap = 0;
-};
-template <int K, int CK>
-cudaError_t sweep_attrs(int dev) {
-    constexpr int kMaxDev = 64;
-    static std::mutex mu;
-    static bool done[kMaxDev] = {};
-    if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
-    std::lock_guard<std::mutex> g(mu);
-    if (done[dev]) return cudaSuccess;
-    const int smem = int(Geom<K, CK>::TOTAL * sizeof(float));
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<K, true, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    // the largest shared-memory carveout: the rings, not L1, bound the resident warps
-    e = cudaFuncSetAttribute(sweep_kernel<K, true, CK>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    done[dev] = true;
-    return cudaSuccess;
-}
-
+// Per-device launch state: the function attributes (both chunk widths) and
+// the resident-warp capacity.
 template <int K>
-cudaError_t sweep_cfg(SweepCfg& out) {
-    constexpr int kMaxDev = 64;
-    static std::mutex mu;
-    static SweepCfg cfg[kMaxDev];
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
-    if ((e = sweep_attrs<K, kChunk>(dev)) != cudaSuccess) return e;
-    if ((e = sweep_attrs<K, 4>(dev)) != cudaSuccess) return e;
-    std::lock_guard<std::mutex> g(mu);
-    if (!cfg[dev].grid_cap) {
+cudaError_t sweep_grid_cap(int& cap) {
+    static PerDevice<int> cfg;
+    return cfg.get(cap, [](int dev, int& v) {
+        const int sm4 = int(Geom<K, 4>::TOTAL * sizeof(float)), sm16 = int(Geom<K, kChunk>::TOTAL * sizeof(float));
+        cudaError_t e = cudaFuncSetAttribute(sweep_kernel<K, true, kChunk>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm16);
+        // the largest shared-memory carveout: the rings, not L1, bound the resident warps
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(sweep_kernel<K, true, kChunk>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(sweep_kernel<K, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(sweep_kernel<K, true, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         int sms = 0, per_sm = 0;
-        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<K, true, kChunk>, 32,
-                                                          size_t(Geom<K, kChunk>::TOTAL) * sizeof(float));
-        if (e != cudaSuccess) return e;
-        cfg[dev].grid_cap = std::max(1, sms * std::max(1, per_sm));
-    }
-    out = cfg[dev];
-    return cudaSuccess;
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<K, true, kChunk>, 32, size_t(sm16));
+        v = std::max(1, sms * std::max(1, per_sm));
+        return e;
+    });
 }
 
 // Launches whose (band, channel) items all fit on the GPU at once are
@@ -935,11 +911,11 @@ cudaError_t sweep_cfg(SweepCfg& out) {
 // shorter hand-over lag); throughput launches poll 16-column chunks.
 template <int K>
 cudaError_t launch_sweep_k(const SweepArgs& A, cudaStream_t s) {
-    SweepCfg c;
-    cudaError_t e = sweep_cfg<K>(c);
+    int cap = 0;
+    cudaError_t e = sweep_grid_cap<K>(cap);
     if (e != cudaSuccess) return e;
-    const int grid = std::max(1, std::min(A.total, c.grid_cap));
-    if (A.total <= c.grid_cap)
+    const int grid = std::max(1, std::min(A.total, cap));
+    if (A.total <= cap)
         sweep_kernel<K, true, 4><<<grid, 32, size_t(Geom<K, 4>::TOTAL) * sizeof(float), s>>>(A);
     else
         sweep_kernel<K, true, kChunk><<<grid, 32, size_t(Geom<K, kChunk>::TOTAL) * sizeof(float), s>>>(A);

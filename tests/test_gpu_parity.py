@@ -583,3 +583,29 @@ def test_k4_throughput_launch_vs_oracle(fgm, cuda, orc, oracle_mod):
         of, ob = orc.ml_solve(imgs[i].double().numpy(), alps[i].double().numpy(), p)
         assert_close(f"K4 batch fg {i}", outs[i][0].double().cpu().numpy(), of)
         assert_close(f"K4 batch bg {i}", outs[i][1].double().cpu().numpy(), ob)
+
+
+# ---- caller-supplied outputs are validated before any device write ----------
+@pytest.mark.gpu
+def test_bad_outputs_rejected(fgm, cuda):
+    from paper_2006_14970_b200 import synth
+
+    img, a = synth.make_composite(64, 48, 11, 2, 3.0)
+    img, a = img.to(cuda), a.to(cuda)
+    good = (torch.empty_like(img), torch.empty_like(img))
+    for bad in ((torch.empty(3, 48, 63, device=cuda), good[1]),                # wrong shape
+                (torch.empty(3, 48, 64, device=cuda, dtype=torch.float64), good[1]),  # wrong dtype
+                (torch.empty(3, 64, 48, device=cuda).transpose(1, 2), good[1]),  # not contiguous
+                (torch.empty(3, 48, 64), good[1])):                             # host tensor
+        with pytest.raises(ValueError):
+            fgm.batch_solve_cuda([img], [a], fgm.BASELINE_PARAMS, outputs=[bad])
+    with pytest.raises(ValueError):
+        fgm.batch_solve_host([img.cpu()], [a.cpu()], fgm.BASELINE_PARAMS,
+                             outputs=[(torch.empty(3, 48, 64), torch.empty(3, 47, 64))])
+    with pytest.raises(ValueError):
+        fgm.ml_foreground_background_levels_cuda(img, a[:, :10], fgm.BASELINE_PARAMS)
+    with pytest.raises(ValueError):
+        fgm.sweep_passes_cuda(img, a, img[:, :10], img, 2, 1e-5, 1.0)
+    out = fgm.batch_solve_cuda([img], [a], fgm.BASELINE_PARAMS, outputs=[good])
+    assert out[0][0] is good[0]
+    fgm.release_memory()
