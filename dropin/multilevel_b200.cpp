@@ -23,10 +23,12 @@ void raise(int rc) {
     if (rc != FGM_OK) throw std::runtime_error(fgm_last_error());
 }
 
-// One pixel on the host (test helper; multilevel.cpp:48-79 contract): the
-// 2x2 system solved in the cancellation-free form of DESIGN.md section 4, in
-// fp64.  Errors as the reference: invalid_argument for bad parameters or
-// neighbour lists, runtime_error for a singular system.
+// One pixel on the host (test helper; multilevel.cpp:48-79 contract), through
+// the reference header's own PixelSystem (multilevel.hpp:45-75: init, one
+// add_neighbor per neighbour, determinant, solve_raw with 1 / det), so the
+// result is bitwise the reference's.  Errors as the reference:
+// invalid_argument for bad parameters or neighbour lists, runtime_error for a
+// singular system.
 PixelSolution solve_one(double ai, const std::array<double, 3>& in, const std::vector<double>& na,
                         const std::vector<std::array<double, 3>>& nf, const std::vector<std::array<double, 3>>& nb,
                         const MlParams& params, bool clamp) {
@@ -34,34 +36,20 @@ PixelSolution solve_one(double ai, const std::array<double, 3>& in, const std::v
     const std::size_t n = na.size();
     if (n < 1) throw std::invalid_argument("solve_pixel: at least one neighbor required");
     if (nf.size() != n || nb.size() != n) throw std::invalid_argument("solve_pixel: neighbor lists must share length");
-    const double u0 = ai, u1 = 1.0 - ai;
-    double S = 0.0;
-    std::array<double, 3> SF{0, 0, 0}, SB{0, 0, 0};
-    for (std::size_t j = 0; j < n; ++j) {
-        const double d = params.eps_r + params.omega * std::abs(ai - na[j]);
-        S += d;
-        for (int c = 0; c < 3; ++c) {
-            SF[std::size_t(c)] += d * nf[j][std::size_t(c)];
-            SB[std::size_t(c)] += d * nb[j][std::size_t(c)];
-        }
-    }
-    const double det = (u0 * u0 + S) * (u1 * u1 + S) - (u0 * u1) * (u0 * u1);
+    PixelSystem sys;
+    sys.init(ai, in.data());
+    for (std::size_t j = 0; j < n; ++j)
+        sys.add_neighbor(params.eps_r + params.omega * std::abs(ai - na[j]), nf[j].data(), nb[j].data());
+    const double det = sys.determinant();
     if (!(det > 0.0) || !std::isfinite(1.0 / det))
         throw std::runtime_error("solve_pixel: singular 2x2 system (det = " + std::to_string(det) + ")");
-    const double D = u0 * u0 + u1 * u1 + S;
-    const double A = (1.0 + u1 * u1 / S) / D, A2 = (1.0 + u0 * u0 / S) / D, Bc = -(u0 * u1) / (S * D);
     PixelSolution sol;
-    for (int c = 0; c < 3; ++c) {
-        const std::size_t k = std::size_t(c);
-        double f = A * SF[k] + Bc * SB[k] + u0 / D * in[k];
-        double b = A2 * SB[k] + Bc * SF[k] + u1 / D * in[k];
-        if (clamp) {
-            f = clamp01(f);
-            b = clamp01(b);
+    sys.solve_raw(1.0 / det, sol.fg.data(), sol.bg.data());
+    if (clamp)
+        for (int c = 0; c < 3; ++c) {
+            sol.fg[std::size_t(c)] = clamp01(sol.fg[std::size_t(c)]);
+            sol.bg[std::size_t(c)] = clamp01(sol.bg[std::size_t(c)]);
         }
-        sol.fg[k] = f;
-        sol.bg[k] = b;
-    }
     return sol;
 }
 

@@ -69,18 +69,22 @@ struct PyrJob {
 inline int pyramid_tiles(int W, int H) { return ((W + kPyrTW - 1) / kPyrTW) * ((H + kPyrTH - 1) / kPyrTH); }
 cudaError_t launch_pyramid(const PyrJob* jobs_dev, int njobs, long long total_tiles, cudaStream_t s);
 
-// ---- K4: coarse levels, one CTA per image, shared-memory resident ---------
+// ---- K4: coarse levels, one CTA per image, shared-memory resident, fp64 ----
 constexpr int kMaxCoarseLevels = 24;
-constexpr int kCoarseCap = 2048;  // max pixels of a level handled by K4
+constexpr int kCoarseCap = 1024;  // max pixels of a level handled by K4 (every level with max(w, h) <= 32)
 
 struct CoarseJob {
     const float* img;  // full-res, 3 planes
     const float* alpha;
+    const double* img64;  // optional fp64 full-res input (the fp64 host path), used instead of img/alpha
+    const double* alpha64;
     int W, H;
     int nlev;
     int lw[kMaxCoarseLevels], lh[kMaxCoarseLevels], lit[kMaxCoarseLevels];
     float* fg_out;  // last coarse level F (3 planes)
     float* bg_out;
+    double* fg_out64;  // optional: the same in fp64 (fp64 host path, image entirely coarse)
+    double* bg_out64;
     int out_pitch;         // row stride of fg_out / bg_out
     long long out_pstride; // plane stride of fg_out / bg_out
     float* lvl_fg[kMaxCoarseLevels];  // optional per-level dumps (debug API)
@@ -141,7 +145,7 @@ cudaError_t launch_metrics(const float* est, const float* gt, const float* alpha
                            const double* kern, int r, double* partial, int blocks, cudaStream_t s);
 cudaError_t launch_compose(const float* fg, const float* bg, const float* alpha, long long n, int nch, float* out,
                            cudaStream_t s);  // scale within the staged window
-cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float omega, cudaStream_t s);
+cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, double eps, double omega, cudaStream_t s);
 // order_dev[t] = (job, 3 * band + channel) of ticket t, band-major across jobs.
 // ticket: the launch's zeroed ticket counter; abort_flag: a zeroed per-launch
 // int (a timed-out boundary-stream wait sets it and every waiter gives up);

@@ -660,47 +660,100 @@ cudaError_t launch_compose(const float* fg, const float* bg, const float* alpha,
 }
 
 // ============================================================================
-// K4: coarse levels.  One CTA per image.  Per level: resample I/alpha from
-// full-res (global) and F/B from the previous level (shared), then
+// K4: coarse levels, in fp64 with the reference's own operation order, so the
+// coarse prefix of every solve is bitwise the reference's (given the same
+// inputs).  One CTA per image.  Per level: I/alpha resampled from the
+// full-resolution input (global; fp64 when the caller passed fp64, else the
+// fp32 input upcast exactly), F/B from the previous level (shared), then
 // `iterations` sweeps in place in shared memory along the wavefront
-// t = x + y + 2k (pixel (x,y) of sweep k depends only on step t-1 values;
-// pixels updated in one step are never read in that step -- DESIGN.md).
+// t = x + y + 2k: pixel (x,y) of sweep k reads only values of step t-1 or
+// earlier, and pixels updated in one step never read each other (equal x + y
+// parity) -- the same values the sequential scanline sweep reads
+// (multilevel.cpp:91-120).  No FMA contraction anywhere (__d*_rn): the
+// reference is built with -ffp-contract=off (CMakeLists.txt:23-24).
 // ============================================================================
 constexpr int kCoarseThreads = 256;
 
-size_t coarse_smem_bytes() { return size_t(16) * kCoarseCap * sizeof(float); }
+// I (3) + alpha + two F/B buffers (6 each), fp64
+size_t coarse_smem_bytes() { return size_t(16) * kCoarseCap * sizeof(double); }
 
-__device__ __forceinline__ void coarse_update(float* __restrict__ sI, float* __restrict__ sA, float* __restrict__ fb,
-                                              int x, int y, int w, int h, float eps, float omega) {
-    const int n = w * h;
-    const int i = y * w + x;
-    const int jL = x > 0 ? i - 1 : i, jR = x < w - 1 ? i + 1 : i;
-    const int jU = y > 0 ? i - w : i, jD = y < h - 1 ? i + w : i;
-    float I[3];
-    float L[6], R[6], U[6], D[6], out[6];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) I[c] = sI[c * n + i];
-    const Coef co = pixel_coef(sA[i], sA[jL], sA[jR], sA[jU], sA[jD], I, eps, omega);
-#pragma unroll
-    for (int p = 0; p < 6; ++p) {
-        L[p] = fb[p * n + jL];
-        R[p] = fb[p * n + jR];
-        U[p] = fb[p * n + jU];
-        D[p] = fb[p * n + jD];
-    }
-    pixel_apply(co, L, R, U, D, out);
-#pragma unroll
-    for (int p = 0; p < 6; ++p) fb[p * n + i] = out[p];
+__device__ __forceinline__ double dclamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+// image.cpp:98-102: top = a + t (b - a), bot = c + t (d - c), clamp01(top + ty (bot - top))
+__device__ __forceinline__ double dbilerp(double a, double b, double c, double d, double tx, double ty) {
+    const double top = __dadd_rn(a, __dmul_rn(tx, __dsub_rn(b, a)));
+    const double bot = __dadd_rn(c, __dmul_rn(tx, __dsub_rn(d, c)));
+    return dclamp01(__dadd_rn(top, __dmul_rn(ty, __dsub_rn(bot, top))));
 }
 
-__global__ void __launch_bounds__(kCoarseThreads) coarse_kernel(const CoarseJob* __restrict__ jobs, float eps,
-                                                                 float omega) {
-    extern __shared__ float sm[];
+// make_taps (image.cpp:71-83) with t kept in fp64
+struct Tap64 {
+    int i0, i1;
+    double t;
+};
+__device__ __forceinline__ Tap64 make_tap64(int d, int src, double scale) {
+    double f = __dadd_rn(__dmul_rn(__dadd_rn(double(d), 0.5), scale), -0.5);
+    if (f < 0.0) f = 0.0;
+    const double max_f = double(src - 1);
+    if (f > max_f) f = max_f;
+    const int i0 = int(f);
+    return {i0, min(i0 + 1, src - 1), __dsub_rn(f, double(i0))};
+}
+
+// One pixel of sweep (multilevel.cpp:93-118), PixelSystem's order
+// (multilevel.hpp:45-75): init, the four clamped neighbours L, R, U, D, the
+// adjugate solve with inv_det = 1 / det, clamp01.
+__device__ __forceinline__ void coarse_update(const double* __restrict__ sI, const double* __restrict__ sA,
+                                              double* __restrict__ fb, int x, int y, int w, int h, double eps,
+                                              double omega) {
+    const int n = w * h;
+    const int i = y * w + x;
+    const int jn[4] = {x > 0 ? i - 1 : i, x < w - 1 ? i + 1 : i, y > 0 ? i - w : i, y < h - 1 ? i + w : i};
+    const double ai = sA[i];
+    const double u0 = ai, u1 = __dsub_rn(1.0, ai);
+    double diag0 = __dmul_rn(u0, u0), diag1 = __dmul_rn(u1, u1);
+    const double off = __dmul_rn(u0, u1);
+    double rf[3], rb[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double Ic = sI[c * n + i];
+        rf[c] = __dmul_rn(Ic, u0);
+        rb[c] = __dmul_rn(Ic, u1);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int j = jn[t];
+        const double dalpha = __dadd_rn(eps, __dmul_rn(omega, fabs(__dsub_rn(ai, sA[j]))));
+        diag0 = __dadd_rn(diag0, dalpha);
+        diag1 = __dadd_rn(diag1, dalpha);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            rf[c] = __dadd_rn(rf[c], __dmul_rn(dalpha, fb[c * n + j]));
+            rb[c] = __dadd_rn(rb[c], __dmul_rn(dalpha, fb[(3 + c) * n + j]));
+        }
+    }
+    const double inv_det = __ddiv_rn(1.0, __dsub_rn(__dmul_rn(diag0, diag1), __dmul_rn(off, off)));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        fb[c * n + i] = dclamp01(__dmul_rn(__dsub_rn(__dmul_rn(diag1, rf[c]), __dmul_rn(off, rb[c])), inv_det));
+        fb[(3 + c) * n + i] = dclamp01(__dmul_rn(__dsub_rn(__dmul_rn(diag0, rb[c]), __dmul_rn(off, rf[c])), inv_det));
+    }
+}
+
+// the full-resolution input value of plane c (3 = alpha) at index k
+__device__ __forceinline__ double full_res(const CoarseJob& J, int c, long long k, long long fps) {
+    if (J.img64) return c < 3 ? J.img64[c * fps + k] : J.alpha64[k];
+    return double(c < 3 ? __ldg(J.img + c * fps + k) : __ldg(J.alpha + k));
+}
+
+__global__ void __launch_bounds__(kCoarseThreads) coarse_kernel(const CoarseJob* __restrict__ jobs, double eps,
+                                                                 double omega) {
+    extern __shared__ double smd[];
     const CoarseJob& J = jobs[blockIdx.x];
     const int cap = kCoarseCap;
-    float* sI = sm;
-    float* sA = sm + 3 * cap;
-    float* sFB[2] = {sm + 4 * cap, sm + 10 * cap};
+    double* sI = smd;
+    double* sA = smd + 3 * cap;
+    double* sFB[2] = {smd + 4 * cap, smd + 10 * cap};
     const int W = J.W, H = J.H;
     const long long fps = (long long)W * H;
     int pw = 1, ph = 1;
@@ -708,26 +761,26 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_kernel(const CoarseJob*
     for (int l = 0; l < nlev; ++l) {
         const int w = J.lw[l], h = J.lh[l], K = J.lit[l];
         const int n = w * h, pn = pw * ph;
-        float* cur = sFB[l & 1];
-        const float* prv = sFB[(l & 1) ^ 1];
+        double* cur = sFB[l & 1];
+        const double* prv = sFB[(l & 1) ^ 1];
         const bool ident = (w == W && h == H);
         const bool same = (w == pw && h == ph);
         const double sxf = __ddiv_rn(double(W), double(w)), syf = __ddiv_rn(double(H), double(h));
         const double sxp = __ddiv_rn(double(pw), double(w)), syp = __ddiv_rn(double(ph), double(h));
         for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
             const int y = idx / w, x = idx - y * w;
-            if (ident) {  // the last level resamples the original: identity copy
+            if (ident) {  // the last level resamples the original: identity copy (image.cpp:116,127)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) sI[c * n + idx] = J.img[c * fps + idx];
-                sA[idx] = J.alpha[idx];
+                for (int c = 0; c < 3; ++c) sI[c * n + idx] = full_res(J, c, idx, fps);
+                sA[idx] = full_res(J, 3, idx, fps);
             } else {
-                const Tap tx = make_tap_s(x, W, sxf), ty = make_tap_s(y, H, syf);
+                const Tap64 tx = make_tap64(x, W, sxf), ty = make_tap64(y, H, syf);
                 const long long r0 = (long long)ty.i0 * W, r1 = (long long)ty.i1 * W;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    const float* s = c < 3 ? J.img + c * fps : J.alpha;
-                    const float v = bilerp(__ldg(s + r0 + tx.i0), __ldg(s + r0 + tx.i1), __ldg(s + r1 + tx.i0),
-                                           __ldg(s + r1 + tx.i1), tx.t, ty.t);
+                    const double v = dbilerp(full_res(J, c, r0 + tx.i0, fps), full_res(J, c, r0 + tx.i1, fps),
+                                             full_res(J, c, r1 + tx.i0, fps), full_res(J, c, r1 + tx.i1, fps), tx.t,
+                                             ty.t);
                     if (c < 3)
                         sI[c * n + idx] = v;
                     else
@@ -736,17 +789,17 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_kernel(const CoarseJob*
             }
             if (l == 0) {  // F, B start as 1x1 zeros (multilevel.cpp:155-156)
 #pragma unroll
-                for (int p = 0; p < 6; ++p) cur[p * n + idx] = 0.0f;
+                for (int p = 0; p < 6; ++p) cur[p * n + idx] = 0.0;
             } else if (same) {
 #pragma unroll
                 for (int p = 0; p < 6; ++p) cur[p * n + idx] = prv[p * pn + idx];
             } else {
-                const Tap tx = make_tap_s(x, pw, sxp), ty = make_tap_s(y, ph, syp);
+                const Tap64 tx = make_tap64(x, pw, sxp), ty = make_tap64(y, ph, syp);
                 const int r0 = ty.i0 * pw, r1 = ty.i1 * pw;
 #pragma unroll
                 for (int p = 0; p < 6; ++p) {
-                    const float* s = prv + p * pn;
-                    cur[p * n + idx] = bilerp(s[r0 + tx.i0], s[r0 + tx.i1], s[r1 + tx.i0], s[r1 + tx.i1], tx.t, ty.t);
+                    const double* s = prv + p * pn;
+                    cur[p * n + idx] = dbilerp(s[r0 + tx.i0], s[r0 + tx.i1], s[r1 + tx.i0], s[r1 + tx.i1], tx.t, ty.t);
                 }
             }
         }
@@ -763,24 +816,28 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_kernel(const CoarseJob*
         }
         if (J.lvl_fg[l]) {
             for (int idx = threadIdx.x; idx < 3 * n; idx += blockDim.x) {
-                J.lvl_fg[l][idx] = cur[idx];
-                J.lvl_bg[l][idx] = cur[3 * n + idx];
+                J.lvl_fg[l][idx] = float(cur[idx]);
+                J.lvl_bg[l][idx] = float(cur[3 * n + idx]);
             }
         }
         pw = w;
         ph = h;
     }
-    const float* fin = sFB[(nlev - 1) & 1];
+    const double* fin = sFB[(nlev - 1) & 1];
     const int n = pw * ph;
     for (int idx = threadIdx.x; idx < 3 * n; idx += blockDim.x) {
         const int c = idx / n, i = idx - c * n, y = i / pw, x = i - y * pw;
         const long long o = c * J.out_pstride + (long long)y * J.out_pitch + x;
-        J.fg_out[o] = fin[idx];
-        J.bg_out[o] = fin[3 * n + idx];
+        J.fg_out[o] = float(fin[idx]);
+        J.bg_out[o] = float(fin[3 * n + idx]);
+        if (J.fg_out64) {  // fp64 host path, image entirely coarse: the exact values
+            J.fg_out64[o] = fin[idx];
+            J.bg_out64[o] = fin[3 * n + idx];
+        }
     }
 }
 
-cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, float eps, float omega, cudaStream_t s) {
+cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, double eps, double omega, cudaStream_t s) {
     if (njobs <= 0) return cudaSuccess;
     static PerDevice<int> attr;  // the > 48 KB shared-memory opt-in, per device
     int unused = 0;

@@ -300,7 +300,24 @@ struct ImageIO {
     float* bg;
     float* const* level_fg;  // optional per-level dumps (n levels)
     float* const* level_bg;
+    // fp64 host path (fgm_ml_solve_host_f64): the caller's fp64 input on the
+    // device (the coarse kernel reads it instead of img / alpha) and, for an
+    // image whose every level is coarse, fp64 outputs written by that kernel
+    const double* img64 = nullptr;
+    const double* alpha64 = nullptr;
+    double* fg64 = nullptr;
+    double* bg64 = nullptr;
 };
+
+// Levels handled by the coarse kernel (K4): the schedule's leading levels of
+// at most kCoarseCap pixels.
+int coarse_levels(const std::vector<Level>& lv) {
+    int nc = 0;
+    while (nc < int(lv.size()) && nc < kMaxCoarseLevels &&
+           size_t(lv[size_t(nc)].w) * lv[size_t(nc)].h <= size_t(kCoarseCap))
+        ++nc;
+    return nc;
+}
 
 struct Plan {
     ImageIO io;
@@ -320,9 +337,7 @@ struct Plan {
 void plan_image(Plan& P, const fgm_params* p) {
     P.lv = schedule(P.io.W, P.io.H, p);
     const int n = int(P.lv.size());
-    P.nc = 0;
-    while (P.nc < n && P.nc < kMaxCoarseLevels && size_t(P.lv[size_t(P.nc)].w) * P.lv[size_t(P.nc)].h <= size_t(kCoarseCap))
-        ++P.nc;
+    P.nc = coarse_levels(P.lv);
     if (P.nc == 0) throw RuntimeError("internal: first level exceeds the coarse capacity");
     P.ia_off.assign(size_t(n), 0);
     for (int l = 0; l < n; ++l) {
@@ -521,6 +536,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
     validate(p);
     require_device();
     const float eps = float(p->regularization), omega = float(p->gradient_weight);
+    const double eps64 = p->regularization, omega64 = p->gradient_weight;  // the coarse kernel is fp64
     std::vector<Plan> plans(ios.size());
     for (size_t i = 0; i < ios.size(); ++i) {
         if (!ios[i].img || !ios[i].alpha || !ios[i].fg || !ios[i].bg) throw InvalidArgument("null buffer");
@@ -550,6 +566,8 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             std::memset(&c, 0, sizeof(c));
             c.img = P.io.img;
             c.alpha = P.io.alpha;
+            c.img64 = P.io.img64;
+            c.alpha64 = P.io.alpha64;
             c.W = P.io.W;
             c.H = P.io.H;
             c.nlev = P.nc;
@@ -567,6 +585,8 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             if (P.nc == int(P.lv.size())) {
                 c.fg_out = P.io.fg;
                 c.bg_out = P.io.bg;
+                c.fg_out64 = P.io.fg64;
+                c.bg_out64 = P.io.bg64;
                 c.out_pitch = Lc.w;
             } else {
                 c.out_pitch = level_pitch(Lc.w);
@@ -837,7 +857,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
             case kPyramid: break;  // (side stream only)
             case kCoarse: {
                 ProfScope ps(s, 2, r.bytes);
-                ck(launch_coarse(reinterpret_cast<const CoarseJob*>(djobs + r.job_off), r.njobs, eps, omega, s),
+                ck(launch_coarse(reinterpret_cast<const CoarseJob*>(djobs + r.job_off), r.njobs, eps64, omega64, s),
                    "coarse_kernel");
                 break;
             }
@@ -998,19 +1018,28 @@ static int host_solve_impl(const void* image, const void* alpha, int w, int h, c
         // image + alpha (4 planes) and F + B (6 planes) in fp32; the fp64 path
         // stages the 4 input planes and the 6 output planes in fp64 as well
         A.reserve(al(4 * n * sizeof(float)) + al(6 * n * sizeof(float)) +
-                      (f64 ? al(6 * n * sizeof(double)) + al(6 * n * sizeof(double)) : 0),
+                      (f64 ? al(4 * n * sizeof(double)) + al(6 * n * sizeof(double)) : 0),
                   s);
         float* dimg = A.take<float>(4 * n);  // 3 image planes + alpha
         float* dout = A.take<float>(6 * n);
         if (f64) {
-            double* staging = A.take<double>(6 * n);
+            double* staging = A.take<double>(4 * n);
+            double* out64 = A.take<double>(6 * n);
             ck(cudaMemcpyAsync(staging, image, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
             ck(cudaMemcpyAsync(staging + 3 * n, alpha, n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
             ck(launch_f64_to_f32(staging, dimg, 4 * n, s), "f64_to_f32");
-            std::vector<ImageIO> io{{dimg, dimg + 3 * n, w, h, dout, dout + 3 * n, nullptr, nullptr}};
+            // the coarse levels read the fp64 input itself (bitwise the
+            // reference's coarse levels); an image that is coarse at every
+            // level gets its fp64 result straight from the coarse kernel
+            ImageIO one{dimg, dimg + 3 * n, w, h, dout, dout + 3 * n, nullptr, nullptr};
+            one.img64 = staging;
+            one.alpha64 = staging + 3 * n;
+            one.fg64 = out64;
+            one.bg64 = out64 + 3 * n;
+            std::vector<ImageIO> io{one};
             solve_batch(io, p, s);
-            double* out64 = A.take<double>(6 * n);
-            ck(launch_f32_to_f64(dout, out64, 6 * n, s), "f32_to_f64");
+            const std::vector<Level> lv = schedule(w, h, p);
+            if (coarse_levels(lv) != int(lv.size())) ck(launch_f32_to_f64(dout, out64, 6 * n, s), "f32_to_f64");
             ck(cudaMemcpyAsync(fg, out64, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
             ck(cudaMemcpyAsync(bg, out64 + 3 * n, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
         } else {

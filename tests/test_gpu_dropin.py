@@ -4,11 +4,11 @@ against the C++ drop-in dropin/multilevel_b200.cpp, i.e. run through the B200
 path.  Expected failures:
   * "level sizes at most double ..." fails in the reference itself
     (test_multilevel.cpp:47-66; SURVEY.md 4) -- it does not call the solver;
-  * "one-pixel image matches iterated solve_pixel" demands bitwise equality of
-    the fp32 GPU solve with the fp64 host solve_pixel (test_multilevel.cpp:
-    208-237); tests/test_gpu_parity.py checks the same case to 1e-6.
-Everything else, including the bitwise exchange-symmetry, permutation and
-determinism cases, must pass."""
+Everything else must pass, including the bitwise exchange-symmetry,
+permutation and determinism cases and "one-pixel image matches iterated
+solve_pixel" (test_multilevel.cpp:208-237: a 1x1 image is coarse at every
+level, so the fp64 coarse kernel, fed the fp64 input by the drop-in, must
+reproduce the reference's arithmetic bitwise)."""
 import os
 import subprocess
 
@@ -19,7 +19,7 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 BIN = os.path.join(ROOT, "dropin", "_build", "ref_tests_b200")
-EXPECTED_FAIL = {"level sizes at most double, exhaustively to 4096", "one-pixel image matches iterated solve_pixel"}
+EXPECTED_FAIL = {"level sizes at most double, exhaustively to 4096"}
 
 
 def test_reference_unit_tests_through_dropin(cuda):

@@ -137,6 +137,28 @@ def test_per_level_vs_oracle(fgm, cuda, orc, oracle_mod, w, h):
     assert np.array_equal(lf[-1].cpu().numpy(), f.cpu().numpy())
 
 
+@pytest.mark.parametrize("w,h,params", [(300, 200, "baseline"), (1920, 1080, "baseline"), (3000, 2000, "defaults"),
+                                        (77, 333, "baseline"), (31, 17, "defaults"), (1, 1, "baseline")])
+def test_coarse_levels_bitwise_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, params):
+    """The coarse levels (every level up to small_size) run in fp64 with the
+    reference's operation order (kernels.cu K4): given the same (fp32)
+    inputs, each coarse level's F/B is the reference's fp64 value rounded
+    to fp32 -- bitwise."""
+    from paper_2006_14970_b200 import synth
+
+    img, a = synth.make_composite(w, h, 91 + w, 5, 4.0)
+    p = oracle_mod.Params(omega=1.0, eps_r=1e-5, iters_high=2) if params == "baseline" else oracle_mod.Params()
+    _, _, lf, lb = fgm.ml_foreground_background_levels_cuda(img.to(cuda), a.to(cuda), params_from(fgm, p))
+    torch.cuda.synchronize()
+    _, _, olf, olb = orc.ml_solve(img.double().numpy(), a.double().numpy(), p, levels=True)
+    sched = orc.level_schedule(w, h, p)
+    n_coarse = sum(1 for (lw, lh, _) in sched if lw * lh <= 1024 and max(lw, lh) <= p.low_res_threshold)
+    assert n_coarse >= 1
+    for l in range(n_coarse):
+        assert np.array_equal(lf[l].cpu().numpy(), olf[l].astype(np.float32)), f"fg level {l} {sched[l]}"
+        assert np.array_equal(lb[l].cpu().numpy(), olb[l].astype(np.float32)), f"bg level {l} {sched[l]}"
+
+
 # ---- single level: K fused sweeps vs `iterations` oracle sweeps ---------------
 @pytest.mark.parametrize("w,h,K", [(37, 29, 1), (64, 64, 2), (100, 70, 3), (130, 97, 4), (50, 40, 8), (33, 200, 10),
                                    (1, 50, 2), (50, 1, 2), (300, 33, 2), (257, 129, 2)])
