@@ -434,6 +434,9 @@ struct StepCtx {
     float* BO;
     int opitch;
     float eps, omega;
+#ifdef FGM_N1_PROBE
+    float probe_zero, probe_ty;
+#endif
 };
 
 // One wavefront step.  G: a pixel of this step or the next may be on the
@@ -511,6 +514,33 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
         if (k == 0) {
             R = make_float2(lds(rc + ring<K>(Gm::OFF_F, 0, 1 + Gm::SH)), lds(rc + ring<K>(Gm::OFF_B, 0, 1 + Gm::SH)));
             D = make_float2(lds(rc + ring<K>(Gm::OFF_F, 1, Gm::SH)), lds(rc + ring<K>(Gm::OFF_B, 1, Gm::SH)));
+#ifdef FGM_N1_PROBE
+            // Cost probe of an in-sweep F/B upsample ("N1"): per step each
+            // lane gathers the 4 taps of F and B of its R pixel from a previous-level
+            // ring, reads an x-tap weight, interpolates (bilerp2), shuffles the result
+            // down as the upper lane's D, and lane 31 interpolates its own D from a
+            // second row pair.  Results are unchanged (added times a runtime zero).
+            {
+                const float tx = lds(rc + ring<K>(Gm::OFF_A, K, Gm::SH + 1));
+                const float2 a0 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 0, Gm::SH)), lds(rc + ring<K>(Gm::OFF_B, 0, Gm::SH)));
+                const float2 a1 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 0, Gm::SH + 2)), lds(rc + ring<K>(Gm::OFF_B, 0, Gm::SH + 2)));
+                const float2 c0 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 1, Gm::SH + 1)), lds(rc + ring<K>(Gm::OFF_B, 1, Gm::SH + 1)));
+                const float2 c1 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 1, Gm::SH + 2)), lds(rc + ring<K>(Gm::OFF_B, 1, Gm::SH + 2)));
+                const float2 v = bilerp2(a0, a1, c0, c1, tx, x_.probe_ty);
+                float2 dv;
+                dv.x = __shfl_down_sync(kFull, v.x, 1);
+                dv.y = __shfl_down_sync(kFull, v.y, 1);
+                if (lane == 31) {
+                    const float2 e0 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 2, Gm::SH)), lds(rc + ring<K>(Gm::OFF_B, 2, Gm::SH)));
+                    const float2 e1 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 2, Gm::SH + 1)), lds(rc + ring<K>(Gm::OFF_B, 2, Gm::SH + 1)));
+                    dv = bilerp2(c0, c1, e0, e1, tx, x_.probe_ty);
+                }
+                R.x = fmaf(x_.probe_zero, v.x, R.x);
+                R.y = fmaf(x_.probe_zero, v.y, R.y);
+                D.x = fmaf(x_.probe_zero, dv.x, D.x);
+                D.y = fmaf(x_.probe_zero, dv.y, D.y);
+            }
+#endif
         } else {
             R = recv[k - 1];
             D = st.outp[k - 1];
@@ -737,6 +767,10 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     cx.opitch = J.opitch;
     cx.eps = eps;
     cx.omega = omega;
+#ifdef FGM_N1_PROBE
+    cx.probe_zero = eps * 0.0f;
+    cx.probe_ty = 0.25f + 0.01f * float(lane);
+#endif
 
     // rows this lane streams
     const RowSrc own = make_rowsrc<K>(J, ch, y0, lane, true, true, true, sbase);
