@@ -134,6 +134,13 @@ int fgm_compose_f32(const float* fg, const float* bg, const float* alpha, int w,
 int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg_in, const float* bg_in, int w,
                          int h, int iterations, double regularization, double gradient_weight, float* fg_out,
                          float* bg_out, void* stream);
+/* The same with the sweep kernel chosen explicitly (parity tests of both):
+ * 0 automatic (as fgm_sweep_passes_f32: one image is a latency-bound launch),
+ * 1 the latency kernel (32-row bands, one row per lane), 2 the throughput
+ * kernel (64-row bands, two rows per lane) that solves batches. */
+int fgm_sweep_passes_kernel_f32(const float* image, const float* alpha, const float* fg_in, const float* bg_in,
+                                int w, int h, int iterations, double regularization, double gradient_weight,
+                                float* fg_out, float* bg_out, int kernel, void* stream);
 
 /* Tuning/debug (process-wide, atomic): 1 computes the I/alpha pyramid of all
  * sub-top levels in one pass over the full-res input (pyramid_kernel), 0

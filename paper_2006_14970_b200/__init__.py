@@ -115,6 +115,8 @@ def _load():
     L.fgm_ml_solve_hwc.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, P, vp, vp, vp]
     L.fgm_sweep_passes_f32.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp, vp,
                                        vp]
+    L.fgm_sweep_passes_kernel_f32.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp,
+                                              vp, C.c_int, vp]
     L.fgm_profile_enable.argtypes = [C.c_int]
     L.fgm_set_pyramid_mode.argtypes = [C.c_int]
     L.fgm_set_debug_guards.argtypes = [C.c_int]
@@ -520,8 +522,10 @@ def compose_cuda(fg, bg, alpha, out=None):
     return out
 
 
-def sweep_passes_cuda(image, alpha, fg, bg, iterations: int, eps_r: float, omega: float):
-    """`iterations` exact Gauss-Seidel sweeps of one level (multilevel.cpp:81-121)."""
+def sweep_passes_cuda(image, alpha, fg, bg, iterations: int, eps_r: float, omega: float, kernel: int = 0):
+    """`iterations` exact Gauss-Seidel sweeps of one level (multilevel.cpp:81-121).
+    kernel: 0 automatic, 1 latency kernel (32-row bands), 2 throughput kernel
+    (64-row bands, the one that solves batches)."""
     import torch
 
     image = _dev_f32(image, "image")
@@ -532,9 +536,9 @@ def sweep_passes_cuda(image, alpha, fg, bg, iterations: int, eps_r: float, omega
     h, w = image.shape[1], image.shape[2]
     fo, bo = torch.empty_like(fg), torch.empty_like(bg)
     with _on(image.device):
-        _check(_load().fgm_sweep_passes_f32(image.data_ptr(), alpha.data_ptr(), fg.data_ptr(), bg.data_ptr(), w, h,
-                                            int(iterations), float(eps_r), float(omega), fo.data_ptr(),
-                                            bo.data_ptr(), _stream_ptr(image.device)))
+        _check(_load().fgm_sweep_passes_kernel_f32(image.data_ptr(), alpha.data_ptr(), fg.data_ptr(), bg.data_ptr(),
+                                                   w, h, int(iterations), float(eps_r), float(omega), fo.data_ptr(),
+                                                   bo.data_ptr(), int(kernel), _stream_ptr(image.device)))
     return fo, bo
 
 

@@ -92,7 +92,9 @@ struct CoarseJob {
 };
 
 // ---- K3: big-level sweep, skewed-band wavefront ---------------------------
-constexpr int kBandRows = 32;   // one warp = 32 skewed rows
+constexpr int kBandRows = 64;     // throughput kernel (sweep.cu): one warp = 64 skewed rows, two per lane
+constexpr int kLatBandRows = 32;  // latency kernel (sweep_lat.cu): one warp = 32 skewed rows, one per lane
+constexpr int kLatMaxJobs = 4;    // launches of at most this many images are chain-bound: latency kernel
 #ifndef FGM_CHUNK
 #define FGM_CHUNK 16
 #endif
@@ -120,12 +122,12 @@ struct SweepJob {
 // sweep streams them with 16-byte cp.async whatever the level width.
 inline int level_pitch(int w) { return (w + 3) & ~3; }
 
-inline int sweep_bands(int h, int K) { return (h + K - 1 + kBandRows - 1) / kBandRows; }
+inline int sweep_bands(int h, int K, int rows = kBandRows) { return (h + K - 1 + rows - 1) / rows; }
 __host__ __device__ inline size_t sweep_stream_len(int w, int K) {
     return (size_t(w + K - 1) * size_t(K) * 2 + 3) / 4 * 4;
 }
-inline size_t sweep_stream_floats(int w, int h, int K) {
-    return size_t(sweep_bands(h, K)) * 3 * sweep_stream_len(w, K);
+inline size_t sweep_stream_floats(int w, int h, int K, int rows = kBandRows) {
+    return size_t(sweep_bands(h, K, rows)) * 3 * sweep_stream_len(w, K);
 }
 // Launch helpers (kernels.cu).  `jobs_dev` are device copies of the arrays.
 // Tiles of 128 x 8 destination pixels; total_tiles = sum over jobs.
@@ -152,6 +154,9 @@ cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, double eps, doub
 // fault_count: a persistent per-device counter of timed-out waits.
 cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
                          float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
+// The same for jobs cut into kLatBandRows-row bands (sweep_lat.cu).
+cudaError_t launch_sweep_lat(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
+                             float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
 extern std::atomic<int> g_sweep_fault;            // debug fault injection (fgm_debug_fault)
 extern std::atomic<long long> g_spin_timeout_ns;  // bound on one boundary-stream wait
 // Fill every job's boundary streams with kStreamSentinel (before its sweep).

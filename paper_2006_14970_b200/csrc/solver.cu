@@ -350,8 +350,10 @@ void plan_image(Plan& P, const fgm_params* p) {
         }
         if (l >= P.nc) {
             for (int K : passes_for(P.lv[size_t(l)].iters)) {
-                P.stream_floats = std::max(P.stream_floats, sweep_stream_floats(P.lv[size_t(l)].w, P.lv[size_t(l)].h, K));
-                P.max_bands = std::max(P.max_bands, sweep_bands(P.lv[size_t(l)].h, K));
+                // (sized for the latency kernel's shorter bands: the larger count)
+                P.stream_floats = std::max(P.stream_floats, sweep_stream_floats(P.lv[size_t(l)].w, P.lv[size_t(l)].h, K,
+                                                                                kLatBandRows));
+                P.max_bands = std::max(P.max_bands, sweep_bands(P.lv[size_t(l)].h, K, kLatBandRows));
             }
             if (passes_for(P.lv[size_t(l)].iters).size() > 1) P.multipass = true;
         }
@@ -438,8 +440,8 @@ struct JobStage {
 // tickets follow S_i + q*lag.  Within an image the order is q ascending (an
 // awaited band always holds an earlier ticket: no deadlock); the tall/wide
 // images' long chains start first instead of forming the launch's tail.
-std::vector<int2> band_order(const std::vector<SweepJob>& sj) {
-    constexpr double lag = kBandRows + kChunk;
+std::vector<int2> band_order(const std::vector<SweepJob>& sj, int rows) {
+    const double lag = rows + kChunk;
     struct Key {
         double k;
         int i, q;
@@ -480,10 +482,11 @@ int read_faults() {
 }
 
 // ticket[0]: the launch's band ticket, ticket[1]: its abort flag (both zeroed)
+// lat: the jobs are cut into kLatBandRows-row bands for the latency kernel
 cudaError_t launch_sweep_passes(int K, const SweepJob* jd, const int2* od, int bands, unsigned* ticket, float eps,
-                                float omega, cudaStream_t s) {
-    return launch_sweep(K, jd, od, 3 * bands, ticket, eps, omega, reinterpret_cast<int*>(ticket + 1),
-                        device_fault_counter(), s);
+                                float omega, bool lat, cudaStream_t s) {
+    return (lat ? launch_sweep_lat : launch_sweep)(K, jd, od, 3 * bands, ticket, eps, omega,
+                                                   reinterpret_cast<int*>(ticket + 1), device_fault_counter(), s);
 }
 
 enum LaunchKind { kCoarse, kResample, kUpsample, kSweep, kCopy, kPyramid };
@@ -497,6 +500,7 @@ struct LaunchRec {
     const void* src = nullptr;
     int side = 0;   // 1: runs on the side stream, then records event `ev`
     int ev = -1;    // side: event to record after; main: event to wait for before
+    int lat = 0;    // kSweep: latency kernel (kLatBandRows-row bands)
 };
 
 // The side stream of the calling thread's device (I/alpha pyramid, which
@@ -731,6 +735,14 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 size_t max_stream = 0;
                 const size_t ticket = st.counters;
                 st.counters += 2;  // ticket, abort flag
+                int njobs = 0;
+                for (auto& a : act) {
+                    const std::vector<int> ps = passes_for(a.P->lv[size_t(a.l)].iters);
+                    njobs += pi < ps.size() && ps[pi] == K ? 1 : 0;
+                }
+                // a few images: the wavefront chain bounds the launch (latency kernel)
+                const bool lat = njobs <= kLatMaxJobs;
+                const int rows = lat ? kLatBandRows : kBandRows;
                 for (auto& a : act) {
                     Plan& P = *a.P;
                     const std::vector<int> ps = passes_for(P.lv[size_t(a.l)].iters);
@@ -769,11 +781,11 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                     J1.stream = P.stream;
                     J1.w = L.w;
                     J1.h = L.h;
-                    J1.nb = sweep_bands(L.h, K);
+                    J1.nb = sweep_bands(L.h, K, rows);
                     J1.band_base = total;
                     J1.vec4 = vec4_ok(J1);
                     total += J1.nb;
-                    max_stream = std::max(max_stream, sweep_stream_floats(L.w, L.h, K));
+                    max_stream = std::max(max_stream, sweep_stream_floats(L.w, L.h, K, rows));
                     sbytes += 64.0 * double(px);
                     sj.push_back(J1);
                 }
@@ -782,8 +794,9 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                     continue;
                 }
                 const size_t off = st.push(sj);
-                const size_t ooff = st.push(band_order(sj));
+                const size_t ooff = st.push(band_order(sj, rows));
                 LaunchRec lr{kSweep, K, int(sj.size()), total, off, ticket, ooff, (long long)max_stream, sbytes};
+                lr.lat = lat ? 1 : 0;
                 if (pi == 0 && has_ia[size_t(j)]) lr.ev = j;  // this step's I/alpha pyramid level
                 if (pi == 0 && pyr_launch && j < J - 1) lr.ev = pyr_ev;
                 launches.push_back(lr);
@@ -880,7 +893,8 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 ProfScope ps(s, 0, r.bytes);
                 const SweepJob* jd = reinterpret_cast<const SweepJob*>(djobs + r.job_off);
                 const int2* od = reinterpret_cast<const int2*>(djobs + r.order_off);
-                ck(launch_sweep_passes(r.K, jd, od, r.total_bands, dctr + r.ticket, eps, omega, s), "sweep_kernel");
+                ck(launch_sweep_passes(r.K, jd, od, r.total_bands, dctr + r.ticket, eps, omega, r.lat != 0, s),
+                   "sweep_kernel");
                 break;
             }
             case kCopy:  // njobs = width, total_bands = rows, max_rows = source pitch (floats)
@@ -1283,9 +1297,19 @@ int fgm_compose_f32(const float* fg, const float* bg, const float* alpha, int w,
 int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg_in, const float* bg_in, int w,
                          int h, int iterations, double regularization, double gradient_weight, float* fg_out,
                          float* bg_out, void* stream) {
+    return fgm_sweep_passes_kernel_f32(image, alpha, fg_in, bg_in, w, h, iterations, regularization, gradient_weight,
+                                       fg_out, bg_out, 0, stream);
+}
+
+int fgm_sweep_passes_kernel_f32(const float* image, const float* alpha, const float* fg_in, const float* bg_in,
+                                int w, int h, int iterations, double regularization, double gradient_weight,
+                                float* fg_out, float* bg_out, int kernel, void* stream) {
     return guarded([&] {
         check_dims(w, h);
         if (iterations < 1) throw InvalidArgument("MlParams: iteration counts must be >= 1");
+        if (kernel < 0 || kernel > 2) throw InvalidArgument("sweep kernel must be 0 (automatic), 1 or 2");
+        const bool lat = kernel != 2;  // one image: latency-bound
+        const int rows = lat ? kLatBandRows : kBandRows;
         fgm_params p{regularization, gradient_weight, 1, 1, 1};
         validate(&p);
         require_device();
@@ -1295,8 +1319,8 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
         size_t sf = 0;
         int mb = 0;
         for (int K : ps) {
-            sf = std::max(sf, sweep_stream_floats(w, h, K));
-            mb = std::max(mb, sweep_bands(h, K));
+            sf = std::max(sf, sweep_stream_floats(w, h, K, rows));
+            mb = std::max(mb, sweep_bands(h, K, rows));
         }
         Arena A;
         A.reserve(al(sf * 4) + al(size_t(3 * mb + 1) * 4) + 2 * al(6 * size_t(px) * 4) + 256 * (ps.size() + 2) +
@@ -1320,20 +1344,21 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
             J1.istride = J1.fstride = J1.ostride = px;
             J1.w = w;
             J1.h = h;
-            J1.nb = sweep_bands(h, ps[pi]);
+            J1.nb = sweep_bands(h, ps[pi], rows);
             J1.band_base = 0;
             J1.vec4 = vec4_ok(J1);
             ck(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned), s), "memset");
             SweepJob* d = A.take<SweepJob>(1);
             ck(cudaMemcpyAsync(d, &J1, sizeof(J1), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
-            const std::vector<int2> ord = band_order({J1});
+            const std::vector<int2> ord = band_order({J1}, rows);
             int2* dord = A.take<int2>(ord.size());
             ck(cudaMemcpyAsync(dord, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice, s),
                "cudaMemcpyAsync(order)");
             ck(launch_stream_fill(d, 1, ps[pi], sf, s), "stream_fill_kernel");
             {
                 ProfScope pr(s, 0, 64.0 * double(px));
-                ck(launch_sweep_passes(ps[pi], d, dord, J1.nb, ctr, float(regularization), float(gradient_weight), s),
+                ck(launch_sweep_passes(ps[pi], d, dord, J1.nb, ctr, float(regularization), float(gradient_weight), lat,
+                                       s),
                    "sweep_kernel");
             }
             fi = J1.fg_out;

@@ -5,47 +5,45 @@
 // Dependency structure.  Pixel (x, y) of sweep k reads
 // L = (x-1, y) and U = (x, y-1) of sweep k, R = (x+1, y), D = (x, y+1) and
 // itself of sweep k-1.  In skewed coordinates u = x + k, v = y + k every one
-// of these is (du, dv) in {(-1,0), (0,-1), (-1,-1)} -- never a positive step
-// -- so:
-//   * a warp owns a band of 32 skewed rows v = 32q + lane and at step t each
-//     lane updates, for every k < K, pixel (t - v - k, v - k);
-//   * every neighbour value comes from the lane itself or from lane-1 one
-//     step earlier (registers + shfl.up), except lane 0, which reads the band
-//     above's last lane from that band's boundary stream in global memory;
-//   * bands depend only on the band above, and are handed out by an atomic
-//     ticket in dependency order (band-major across the images of a launch),
-//     so every awaited band is already resident.
+// of these is (du, dv) in {(-1,0), (0,-1), (-1,-1)} -- never a positive step.
+//
+// Geometry (round 2).  A warp owns a band of 64 skewed rows; lane j owns the
+// two consecutive rows r = 2j, 2j+1 (band-relative) and at step t updates, for
+// every slot k < K, pixel (t - r - k, y0 + r - k) of each row.  Every value a
+// step needs was produced at the previous step: by the same row (L, and D of
+// slot k >= 1), by the row above (U, and R of slot k >= 1) -- for row 2j+1
+// that is row 2j of the same lane, for row 2j the previous lane's row 2j-1
+// (shfl.up), for lane 0 the band above's last row, read from that band's
+// boundary stream.  The 2 x K pixel updates of a step are independent.
+//
+// Coefficients.  The 2x2 matrix depends on alpha only and is common to the
+// three channels and to the K sweeps (multilevel.hpp:37-43): slot k of row
+// 2j+1 updates the pixel slot k-1 of row 2j updated two steps earlier (pixel
+// (x, y) of sweep k runs at step x + y + 2k), so its coefficients are that
+// step's, delayed in registers; only row 2j's slots k >= 1 recompute theirs.  Edge weights are reused along the rows (dL = the
+// previous step's dR) and down the lane (row 2j+1's dU = row 2j's previous dD).
+//
+// Memory staging.  Each warp streams its band's rows of alpha, I_c and the
+// initial F_c, B_c through per-row shared-memory rings of 32 columns, refilled
+// in 16-column (64-byte) row segments: four lanes per row segment, eight row
+// segments per cp.async instruction (per-lane 16-byte segments of 32
+// different rows cap at 2.7 TB/s on B200, 64-byte segments reach 5.8-6.3 TB/s
+// at this kernel's occupancy; profiles/r02/membench*.txt).  A row's next
+// segment is issued as soon as the segment it replaces is no longer read; the
+// row offsets of the two lanes' rows make the refills of a 4-step group fall
+// on 4 consecutive rows of every 16-row block.  Outputs go through a 16-column
+// ring per row and leave as 64-byte row segments (two rows per store).
 //
 // Boundary streams carry no flags: the buffer is filled with a NaN sentinel
-// before the launch, lane 31 of band q stores its K (F_c, B_c) pairs per
-// column, and band q+1 polls each 16-column chunk until no word is the
+// before the launch, lane 31 stores its last row's K (F_c, B_c) pairs per
+// column, and the band below polls each chunk of columns until no word is the
 // sentinel (outputs are clamped to [0, 1], never NaN).  Each word validates
-// itself, so no fences are needed on either side; the next chunk is fetched
-// one chunk ahead and re-polled once per group while incomplete.
-//
-// The three colour channels share only alpha (the 2x2 matrix is common to all
-// channels, multilevel.hpp:37-43), so each (band, channel) is an independent
-// warp: it computes the alpha-only coefficients of its pixels and runs the
-// F_c / B_c recurrence (pixel_apply1) of its channel.  The left edge weight
-// of a pixel is the right edge weight of the pixel the same slot updated one
-// step earlier (|a - b| is exactly symmetric), so only three are computed.
-//
-// Memory: each warp streams its band's rows of alpha, I_c and the initial F_c,
-// B_c through per-row shared-memory rings of 32 columns, filled by cp.async
-// 16-byte blocks M groups ahead of use.  Element (row r, column x) sits at
-// ring column x mod 32; the first MIR columns are mirrored after column 31, so
-// every read of a step is  lane_base + 4*c + (compile-time offset)  with one
-// c = (t - lane - SH) mod 32 per step -- no per-access index arithmetic.  Rows
-// are RS = 32 + MIR floats apart: the diagonal reads of a step hit banks
-// (RS - 1) * lane + const, all distinct since RS - 1 is odd.  Outputs go
-// through a 16-column ring per row and leave as 64-byte row segments (two
-// rows per step) once complete.  Steps run in groups of four: loads, stream
-// chunks and the border/fast decision are handled once per group.
+// itself, so no fences are needed on either side; the waits are bounded
+// (timeout -> error, not a hang).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <atomic>
-#include <mutex>
 
 #include "fgm_device.cuh"
 #include "fgm_internal.h"
@@ -53,15 +51,15 @@
 namespace fgm {
 namespace {
 
+constexpr int R = 2;           // rows per lane
+constexpr int BR = kBandRows;  // band rows
+static_assert(BR == 32 * R, "a band is 32 lanes x R rows");
+
 __device__ __forceinline__ void cp_async16(unsigned sdst, const float* gsrc, int src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sdst), "l"(gsrc), "r"(src_bytes) : "memory");
 }
-// Predicated 16-byte copy without zero-fill (a predicate, not a branch).
-__device__ __forceinline__ void cp_async16_if(unsigned sdst, const float* gsrc, unsigned pred) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p cp.async.cg.shared.global [%0], [%1], 16;\n}" ::"r"(sdst),
-        "l"(gsrc), "r"(pred)
-        : "memory");
+__device__ __forceinline__ void cp_async16f(unsigned sdst, const float* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async4(unsigned sdst, const float* gsrc, int src_bytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sdst), "l"(gsrc), "r"(src_bytes) : "memory");
@@ -80,8 +78,7 @@ __device__ __forceinline__ float4 ld_relaxed_v4(const float* p) {
     return v;
 }
 // Boundary-stream stores need no ordering against this warp's other memory
-// operations (every word validates itself), hence no "memory" clobber: the
-// compiler may keep scheduling shared-memory loads across them.
+// operations (every word validates itself), hence no "memory" clobber.
 __device__ __forceinline__ void st_relaxed_v4(float* p, float4 v) {
     asm volatile("st.relaxed.gpu.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
                  "f"(v.w));
@@ -89,572 +86,442 @@ __device__ __forceinline__ void st_relaxed_v4(float* p, float4 v) {
 __device__ __forceinline__ void st_relaxed_v2(float* p, float2 v) {
     asm volatile("st.relaxed.gpu.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y));
 }
-// The dynamic shared memory of the sweep kernel, addressed by float index:
-// the compiler sees shared-space accesses (LDS/STS with the compile-time part
-// of an index folded into the instruction) and orders them against
-// __syncwarp and the cp.async waits.
 extern __shared__ float4 sweep_sm4[];
 __device__ __forceinline__ float* smf() { return reinterpret_cast<float*>(sweep_sm4); }
 __device__ __forceinline__ float lds(int i) { return smf()[i]; }
-__device__ __forceinline__ void sts(int i, float v) { smf()[i] = v; }
 __device__ __forceinline__ void sts4(int i, float4 v) { reinterpret_cast<float4*>(smf() + i)[0] = v; }
 __device__ __forceinline__ void stg(float* p, float v) { __stcg(p, v); }
 __device__ __forceinline__ bool is_sentinel(float v) { return __float_as_uint(v) == kStreamSentinel; }
-#ifndef FGM_GROUP
-#define FGM_GROUP 4
-#endif
+
 // Shared-memory geometry of one (band, channel) warp, in floats.
-//
-// Ring window.  In row-time tau = x + r (band row r, column x) the reads of
-// step t cover alpha tau in [t-2K+2, t+2] (the next step's pixels and their
-// four neighbours), image [t-2K+3, t+1] and the initial F/B [t, t+1].  Steps
-// run in groups of S = 4; the S-column blocks of every row are issued at
-// the end of each group with a lead L = S*M - 1 + W1 (W1 = the window's reach
-// past the group), so a group waits only for loads issued M groups earlier;
-// the live span S*M + S - 1 + W0 + W1 must fit in the 32 ring columns
-// (static_asserts below).
-template <int K, int CK = kChunk>
+//   rings: [plane][ring row][32 columns], column x at x & 31; ring row = band
+//          row - L_p (alpha rows -K..64, image rows -(K-1)..63, F/B rows 0..64)
+//   output ring: [F/B][orow(r)][16 columns]; chunk buffer: [column][k][F, B]
+// Read window of ring row r at step t, relative to t - r: alpha [MA, 1],
+// image [MI, 0], F/B [0, 1] (MA, MI: the recomputed slots and the rows below
+// reading their upper neighbour).  A 16-column segment is refilled when the
+// segment whose ring slot it takes leaves the window.
+template <int K, int CK>
 struct Geom {
-    static constexpr int RW = 32;               // ring columns
-    static constexpr int SH = K - 1;            // read column shift: offsets d + SH >= 0
-    static constexpr int MIR = K <= 2 ? 4 : 8;  // mirrored columns (> largest shifted offset)
-    static constexpr int RS = RW + MIR;         // row stride (floats), 16-byte multiple, RS - 1 odd
-    // steps per group = columns per load block.  (8 in throughput launches
-    // runs 2% fewer instructions but measured 3% slower on the C4 batch: the
-    // four unrolled 8-step paths no longer share the instruction cache.)
-    static constexpr int S = FGM_GROUP;
-    static constexpr int M = 16 / S;            // load groups in flight
-    static constexpr int L = S * M + 1;         // load lead: S*M - 1 + W1, W1 = 2 (alpha; 1 for the others)
-    static constexpr int NA = 33 + K;           // alpha ring rows: band rows -K .. 32
-    static constexpr int NI = 31 + K;           // image ring rows: band rows -(K-1) .. 31
-    static constexpr int NF = 33;               // F/B ring rows: band rows 0 .. 32
-    static constexpr int OW = 16;               // output ring columns
+    static constexpr int RW = 32;
+    static constexpr int LA = -K, NA = BR + 1 + K;
+    static constexpr int LI = -(K - 1), NI = BR + K - 1;
+    static constexpr int NF = BR + 1;  // F/B rows 0 .. 64
     static constexpr int OFF_A = 0;
-    static constexpr int OFF_I = OFF_A + NA * RS;
-    static constexpr int OFF_F = OFF_I + NI * RS;
-    static constexpr int OFF_B = OFF_F + NF * RS;
-    static constexpr int OFF_O = OFF_B + NF * RS;  // [plane F/B][orow(j)][OW]
-    static constexpr int OPL = 33 * OW;
+    static constexpr int OFF_I = OFF_A + NA * RW;
+    static constexpr int OFF_F = OFF_I + NI * RW;
+    static constexpr int OFF_B = OFF_F + NF * RW;
+    static constexpr int OW = 16;
+    static constexpr int OPL = (BR + BR / 16) * OW;
+    static constexpr int OFF_O = OFF_B + NF * RW;
     static constexpr int OFF_C = OFF_O + 2 * OPL;
-    static constexpr int CH = CK * K * 2;      // one boundary-stream chunk of CK columns: [u][k][F,B]
-    static constexpr int CH4 = CH / 4;         // float4 per chunk (<= 32: one per lane)
+    static constexpr int CH = CK * K * 2;  // one boundary-stream chunk: [column][k][F, B]
+    static constexpr int CH4 = CH / 4;     // float4 per chunk (<= 32: one per lane)
     static constexpr int TOTAL = OFF_C + CH;
-    static_assert(L + (2 * K - 2) + S <= RW, "alpha ring too small for its lead");
-    static_assert(2 + SH <= MIR && MIR % 4 == 0 && RS % 4 == 0, "mirror too narrow");
+    static constexpr int MA = K >= 2 ? -(2 * K - 1) : -1;
+    static constexpr int MI = -2 * (K - 1);
+    static constexpr int MF = 0;
+    // the refill phase of a plane: issue time - free time, making the rows of
+    // a 4-step group's refills 4 consecutive rows of each 16-row block
+    static constexpr int phase(int m) { return ((m % 4) + 4) % 4; }
+    // a group waits for the refills of the group before last (lead >= 2
+    // groups) when every plane's window leaves >= 8 steps, else the last one
+    static constexpr int lead(int m) { return 15 + m - phase(m) - 3; }
+    static constexpr int WAITN = lead(MA) >= 8 && lead(MI) >= 8 ? 1 : 0;
     static_assert(CH % 4 == 0 && CH4 <= 32, "a chunk is at most one float4 per lane");
+    static_assert(MA - 1 >= -RW / 2 && lead(MA) >= 4, "read window too wide for the ring");
 };
 
-// output ring row of band row j (a padding row after row 15: the diagonal
-// writes and the two-row flush reads hit distinct banks)
-__device__ __forceinline__ constexpr int orow(int j) { return j + (j >> 4); }
+__device__ __forceinline__ constexpr int orow(int r) { return r + (r >> 4); }
 
-// The global rows a lane streams into its rings (its own row and, for some
-// lanes, one extra row: alpha -K..-1 and 32, image -(K-1)..-1, F/B 32).
-// Ring rows of one band row sit at compile-time offsets from `s` (alpha row
-// r + K, image row r + K - 1, F/B row r); planes the lane does not stream, or
-// rows outside the image, are masked off in `vm` (their ring slots are never
-// read unclamped).
-struct RowSrc {
-    const float* g[4];  // alpha, image c, F_c, B_c rows (column 0)
-    unsigned s;         // shared address of ring offset 0, ring row r, column 0
-    unsigned vm;        // bit p: plane p is streamed
-    int r;              // row relative to the band
-};
-
-template <int K>
-__device__ __forceinline__ RowSrc make_rowsrc(const SweepJob& J, int ch, int y0, int r, bool doA, bool doI, bool doF,
-                                              unsigned sbase) {
-    using G = Geom<K>;
-    RowSrc rs;
-    const int y = y0 + r;
-    const bool ok = y >= 0 && y < J.h;
-    const long long oi = (long long)(ok ? y : 0) * J.ipitch, of = (long long)(ok ? y : 0) * J.fpitch;
-    rs.g[0] = J.alpha + oi;
-    rs.g[1] = J.img + ch * J.istride + oi;
-    rs.g[2] = J.fg_in + ch * J.fstride + of;
-    rs.g[3] = J.bg_in + ch * J.fstride + of;
-    rs.s = sbase + 4u * unsigned(r * G::RS);  // may wrap below sbase: only ever offset back into range
-    rs.vm = ok ? (doA ? 1u : 0u) | (doI ? 2u : 0u) | (doF ? 12u : 0u) : 0u;
-    rs.r = r;
-    return rs;
-}
-
-// Ring offset (floats) of plane p's row r relative to ring row r of offset 0.
-template <int K>
-__device__ __forceinline__ constexpr int plane_off(int p) {
-    using G = Geom<K>;
-    return p == 0 ? G::OFF_A + K * G::RS : p == 1 ? G::OFF_I + (K - 1) * G::RS : p == 2 ? G::OFF_F : G::OFF_B;
-}
-
-// cp.async of the S-column block at column x0 (S-aligned) of every streamed
-// plane of one row into the rings, as 4-column pieces (each also into the
-// mirror columns when it lands in the first MIR columns).  Columns past the
-// row end are zero-filled (src-size); pieces outside [0, w) are skipped.
-template <int K, bool V4, int CK>
-__device__ __forceinline__ void put_blocks(const RowSrc& rs, int x0, int w) {
-    using G = Geom<K, CK>;
-    if (x0 < 0) return;
-#pragma unroll
-    for (int b = 0; b < G::S / 4; ++b) {
-        const int xb = x0 + 4 * b;
-        if (xb >= w) return;
-        const int nb = min(w - xb, 4) * 4;
-        const int c = xb & (G::RW - 1);
-        const unsigned sc = rs.s + 4u * c;
-        const bool mir = c < G::MIR;
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            if (!(rs.vm & (1u << p))) continue;
-            const float* g = rs.g[p] + xb;
-            const unsigned d = sc + 4u * plane_off<K>(p);
-            if (V4) {
-                cp_async16(d, g, nb);
-                if (mir) cp_async16(d + 4u * G::RW, g, nb);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int ok = 4 * i < nb;
-                    cp_async4(d + 4 * i, ok ? g + i : g, ok ? 4 : 0);
-                    if (mir) cp_async4(d + 4u * G::RW + 4 * i, ok ? g + i : g, ok ? 4 : 0);
-                }
-            }
-        }
-    }
-}
-
-// The block of one row issued at the end of group t4 (lead L).
-template <int K, bool V4, int CK>
-__device__ __forceinline__ void issue_row(const RowSrc& rs, int t4, int w) {
-    using G = Geom<K, CK>;
-    put_blocks<K, V4, CK>(rs, (t4 + G::S + G::L - rs.r) & ~(G::S - 1), w);
-}
-
-// Interior groups of 16-byte-aligned jobs: every lane's block is inside
-// [0, w), so no range checks and no zero-fill; the per-lane plane mask and
-// the mirror copy become instruction predicates.  MASK: compile-time plane
-// mask (15 for a lane's own row of an interior band), else rs.vm.
-template <int K, unsigned MASK, int CK>
-__device__ __forceinline__ void issue_row_fast(const RowSrc& rs, int t4) {
-    using G = Geom<K, CK>;
-    const unsigned x0 = unsigned(t4 + G::S + G::L - rs.r) & ~unsigned(G::S - 1);  // >= 0 in interior groups
-    const unsigned c = x0 & (G::RW - 1);  // S-aligned: the pieces of a block never wrap the ring
-    const unsigned sc = rs.s + 4u * c;
-    const unsigned vm = MASK ? MASK : rs.vm;
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        const float* g = rs.g[p] + x0;
-        const unsigned d = sc + 4u * plane_off<K>(p);
-        const unsigned on = (vm >> p) & 1u;
-#pragma unroll
-        for (int b = 0; b < G::S / 4; ++b) {
-            cp_async16_if(d + 16u * b, g + 4 * b, on);
-            if (4 * b < G::MIR)  // only the first MIR columns of the ring are mirrored
-                cp_async16_if(d + 16u * b + 4u * G::RW, g + 4 * b, on & (c + 4u * b < unsigned(G::MIR) ? 1u : 0u));
-        }
-    }
-}
-
-// Interior groups of interior bands, flattened: the 130 + 2K (plane, band
-// row) blocks a group issues (alpha rows -K..32, image rows -(K-1)..31, F and
-// B rows 0..32) are dealt to the lanes of ceil((130 + 2K) / 32) cp.async
-// instructions instead of one own-row and one extra-row instruction per plane
-// (the extra rows occupy three lanes).  Per lane and instruction: the row's
-// global base, its ring address and its lead q = S + L - r, all fixed per band.
-template <int K>
-struct FlatSrc {
-    static constexpr int N = (130 + 2 * K + 31) / 32;
-    const float* g[N];
-    unsigned s[N];
-    int q[N];
-    unsigned on;  // bit i: lane holds an item in instruction i
-};
-
-template <int K, int CK>
-__device__ __forceinline__ FlatSrc<K> make_flat(const SweepJob& J, int ch, int y0, int lane, unsigned sbase) {
-    using G = Geom<K, CK>;
-    FlatSrc<K> f;
-    f.on = 0;
-    constexpr int NAl = 33 + K, NIm = 31 + K, NFB = 33;
-#pragma unroll
-    for (int i = 0; i < FlatSrc<K>::N; ++i) {
-        int it = 32 * i + lane;
-        int p = 0, r = 0;
-        if (it < NAl) {
-            p = 0;
-            r = it - K;
-        } else if ((it -= NAl) < NIm) {
-            p = 1;
-            r = it - (K - 1);
-        } else if ((it -= NIm) < NFB) {
-            p = 2;
-            r = it;
-        } else if ((it -= NFB) < NFB) {
-            p = 3;
-            r = it;
-        } else {
-            p = -1;
-        }
-        const int y = min(max(y0 + r, 0), J.h - 1);  // (in range for interior bands)
-        const float* base = p == 0 ? J.alpha + (long long)y * J.ipitch
-                          : p == 1 ? J.img + ch * J.istride + (long long)y * J.ipitch
-                          : p == 2 ? J.fg_in + ch * J.fstride + (long long)y * J.fpitch
-                                   : J.bg_in + ch * J.fstride + (long long)y * J.fpitch;
-        f.g[i] = base;
-        const int po = p == 0 ? plane_off<K>(0) : p == 1 ? plane_off<K>(1) : p == 2 ? plane_off<K>(2) : plane_off<K>(3);
-        f.s[i] = sbase + 4u * unsigned(po + r * G::RS);
-        f.q[i] = G::S + G::L - r;
-        if (p >= 0) f.on |= 1u << i;
-    }
-    return f;
-}
-
-template <int K, int CK>
-__device__ __forceinline__ void issue_flat(const FlatSrc<K>& f, int t4) {
-    using G = Geom<K, CK>;
-#pragma unroll
-    for (int i = 0; i < FlatSrc<K>::N; ++i) {
-        const unsigned x0 = unsigned(t4 + f.q[i]) & ~unsigned(G::S - 1);
-        const unsigned c = x0 & (G::RW - 1);
-        const float* g = f.g[i] + x0;
-        const unsigned d = f.s[i] + 4u * c;
-        const unsigned on = (f.on >> i) & 1u;
-#pragma unroll
-        for (int b = 0; b < G::S / 4; ++b) {
-            cp_async16_if(d + 16u * b, g + 4 * b, on);
-            if (4 * b < G::MIR)
-                cp_async16_if(d + 16u * b + 4u * G::RW, g + 4 * b, on & (c + 4u * b < unsigned(G::MIR) ? 1u : 0u));
-        }
-    }
-}
-
-// Everything issued "before group t0".
-template <int K, bool V4, int CK>
-__device__ __forceinline__ void prologue_row(const RowSrc& rs, int t0, int w) {
-    using G = Geom<K, CK>;
-    const int last = (t0 + G::L - rs.r) & ~(G::S - 1);  // the block issued at the end of group t0 - S
-    for (int x0 = 0; x0 <= last; x0 += G::S) put_blocks<K, V4, CK>(rs, x0, w);
-}
-
-// Packed (F, B) arithmetic (FFMA2, fgm_device.cuh) or the scalar form; the
-// two are bitwise identical.
-#ifndef FGM_PACKED
-#define FGM_PACKED 2
-#endif
-#if FGM_PACKED == 2
-using SCoef = CoefR;
-__device__ __forceinline__ SCoef coef_dl(float a, float dL, float aR, float aU, float aD, float I, float eps,
-                                         float omega) {
-    return pixel_coefr_dl(a, dL, aR, aU, aD, I, eps, omega);
-}
-__device__ __forceinline__ float2 apply_coef(const SCoef& co, float2 L, float2 R, float2 U, float2 D) {
-    return pixel_applyr(co, L, R, U, D);
-}
-#elif FGM_PACKED
-using SCoef = CoefP;
-__device__ __forceinline__ SCoef coef_dl(float a, float dL, float aR, float aU, float aD, float I, float eps,
-                                         float omega) {
-    return pixel_coefp_dl(a, dL, aR, aU, aD, I, eps, omega);
-}
-__device__ __forceinline__ float2 apply_coef(const SCoef& co, float2 L, float2 R, float2 U, float2 D) {
-    return pixel_applyp(co, L, R, U, D);
-}
-#else
-using SCoef = Coef1;
-__device__ __forceinline__ SCoef coef_dl(float a, float dL, float aR, float aU, float aD, float I, float eps,
-                                         float omega) {
-    return pixel_coef1_dl(a, dL, aR, aU, aD, I, eps, omega);
-}
-__device__ __forceinline__ float2 apply_coef(const SCoef& co, float2 L, float2 R, float2 U, float2 D) {
-    return pixel_apply1(co, L, R, U, D);
-}
-#endif
-
-// Float offset, from rc = lane_base + c, of ring `off`, ring row lane + row,
-// shifted column offset dp.
-template <int K>
-__device__ __forceinline__ constexpr int ring(int off, int row, int dp) {
-    return off + row * Geom<K>::RS + dp;
-}
-
-// Coefficients of slot k's pixel of the next step (column offset 1 - k from
-// t - lane), its left edge weight `dL` given.  G: clamp neighbours at the
-// image border.
-template <int K, bool G, bool Y = false, bool XL = false>
-__device__ __forceinline__ SCoef next_coef(int rc, int k, float dL, int x, int y, int w, int h, float eps,
-                                           float omega) {
-    using Gm = Geom<K>;
-    const int dp = 1 - k + Gm::SH;  // shifted column of the pixel
-    const int ar = K - k;           // alpha ring row (relative to lane) of the pixel
-    const float a = lds(rc + ring<K>(Gm::OFF_A, ar, dp));
-    float aR = lds(rc + ring<K>(Gm::OFF_A, ar, dp + 1));
-    float aU = lds(rc + ring<K>(Gm::OFF_A, ar - 1, dp));
-    float aD = lds(rc + ring<K>(Gm::OFF_A, ar + 1, dp));
-    const float I = lds(rc + ring<K>(Gm::OFF_I, K - 1 - k, dp));
-    if (G || XL) {
-        if (x <= 0) dL = eps;  // edge_weight(a, a)
-    }
-    if (G) {
-        if (x >= w - 1) aR = a;
-    }
-    if (G || Y) {
-        if (y <= 0) aU = a;
-        if (y >= h - 1) aD = a;
-    }
-    return coef_dl(a, dL, aR, aU, aD, I, eps, omega);
-}
-
-// Coefficients from scratch (the first step of a band: no left pixel yet).
-template <int K>
-__device__ __forceinline__ SCoef first_coef(int rc, int k, int x, int y, int w, int h, float eps, float omega) {
-    using Gm = Geom<K>;
-    const int dp = 1 - k + Gm::SH;
-    const int ar = K - k;
-    const float a = lds(rc + ring<K>(Gm::OFF_A, ar, dp));
-    const float aL = lds(rc + ring<K>(Gm::OFF_A, ar, dp - 1));
-    const float dL = edge_weight(a, x <= 0 ? a : aL, eps, omega);
-    return next_coef<K, true>(rc, k, dL, x, y, w, h, eps, omega);
+// The rank-one coefficients (fgm_device.cuh, pixel_coefr_dl) from the four
+// edge weights: the same operations in the same order.
+__device__ __forceinline__ CoefR coef_w(float a, float dL, float dR, float dU, float dD, float I) {
+    CoefR co;
+    co.dL = dL;
+    co.dR = dR;
+    co.dU = dU;
+    co.dD = dD;
+    const float S = __fadd_rn(__fadd_rn(__fadd_rn(dL, dR), dU), dD);
+    co.u = pk2(a, __fsub_rn(1.0f, a));
+    const float2 uu = upk2(mul2(co.u, co.u));
+    const float Dn = __fadd_rn(__fadd_rn(uu.x, uu.y), S);
+    co.iS = rcp_approx(S);
+    const float iD = rcp_approx(Dn);
+    co.pq = mul2(pk2(iD, iD), co.u);
+    co.I = I;
+    return co;
 }
 
 template <int K>
 struct LaneState {
-    float2 outp[K];   // this lane's (F_c, B_c) outputs of the previous step
-    float2 rprev[K];  // what this lane received from lane-1 at the previous step (border steps)
-    SCoef co[K];      // coefficients of this step's pixels (computed one step ahead)
+    float2 o[R][K];  // (F_c, B_c) of the previous step, per row and slot
+    float2 o2[K];    // row 2j's outputs two steps back (border self values of row 2j+1)
+    float2 rvp[K];   // the previous step's values from the row above row 2j
+    CoefR cp1[K];    // row 2j's coefficients of the previous step
+    CoefR cp2[K];    // and of the step before (row 2j+1's slots 1..K-1)
+    float aRp[R];    // the previous step's right-neighbour alpha per row (this step's alpha)
+    float dRp[R];    // the previous step's slot-0 dR per row (this step's dL)
+    float dDp;       // row 2j's previous slot-0 dD (row 2j+1's dU)
+    float dRr[K];    // row 2j's recomputed slots: the previous dR
+    float aU0p, a0p; // K = 2: the previous step's alpha above row 2j and row 2j's alpha
+    float2 FRp[R];   // the previous step's initial (F, B) right neighbours: this step's slot-0 own values
 };
 
-template <int K>
 struct StepCtx {
-    int lb;  // float index of ring offset 0, row "lane", column 0
-    int ob;  // output ring row orow(lane), column 0
-    int lane, y0, w, h;
+    int lane, y0, w, h, Umax;
+    unsigned lb4;      // byte offset of ring row 2j in a plane (256 * lane: bits >= 8)
+    unsigned ob4;      // byte offset of output-ring row orow(2j) (bits >= 6)
+    unsigned flb4;     // flush: byte offset of output-ring row 17 * (lane >> 4), column lane & 15
     bool has_up, has_down;
-    int Umax;
     float* my_stream;  // this band's stream (column 0)
-    float* FO;  // output planes at band row 0 (image row y0 - (K-1))
-    float* BO;
-    int opitch;
+    float* gF;         // flush base, F plane: FO + 16 (lane >> 4) (opitch - 1) + (lane & 15) - K - 14
+    float* gB;
+    int op1;           // opitch - 1
+    unsigned ytop, ybot;  // YE: bit (i * K + k): pixel row y <= 0 / y >= h - 1 (constant over the band)
     float eps, omega;
-#ifdef FGM_N1_PROBE
-    float probe_zero, probe_ty;
-#endif
 };
 
-// One wavefront step.  G: a pixel of this step or the next may be on the
-// image border (clamped neighbours) or an output row segment may be partial.
-// Y (with G false): interior columns of a band touching row 0 or h-1: only
-// the row clamps and the output row bounds of G (the first band heads every
-// image's chain, so it must not run at border-path speed).
-// XL (with G false): the first steps of a band, where only the left column
-// border occurs (x <= 0): the L clamp and the bounds of the stream and the
-// flush, as selects and predicates.  Every band's start is on the chain's
-// critical path (the band below waits for it).
-// Per-group addressing of the interior paths.  With K = 2 (mod 4) a group's
-// four flushed output rows never cross a 16-row half of the output ring
-// (u = t - (K-1) - 15 starts the group at a multiple of 4), so step s of the
-// group flushes row jf0 + s of segment xs0: the global addresses advance by
-// one output row per step and the ring offsets by one ring row, and lane 31's
-// boundary-stream slot by 2K floats (an immediate offset).
-template <int K>
-struct GroupAddr {
-    float* fo;        // flush address of step 0, F plane
-    float* bo;        // and B plane
-    int o0;           // output-ring float index of step 0
-    bool seg_ok;      // XL: the segment start column is inside the row
-    int jf0;          // flushed band row of step 0
-    float* sdst;      // lane 31's boundary-stream slot of step 0
-};
-template <int K>
-__device__ __forceinline__ constexpr bool group_addr_ok() { return K % 4 == 2; }
-
-template <int K, int CK>
-__device__ __forceinline__ GroupAddr<K> group_addr(const StepCtx<K>& x_, int t4) {
-    using Gm = Geom<K, CK>;
-    constexpr int OW = Gm::OW;
-    GroupAddr<K> g;
-    const int lane = x_.lane;
-    const int col = lane & (OW - 1);
-    const int u0 = t4 - (K - 1) - (OW - 1);
-    g.jf0 = (u0 & (OW - 1)) + (lane & 16);
-    const int xs0 = (u0 & ~(OW - 1)) - (lane & 16);
-    g.seg_ok = xs0 >= 0;
-    const unsigned off = unsigned(g.jf0 * x_.opitch + xs0 + col);  // (used only when seg_ok)
-    g.fo = x_.FO + off;
-    g.bo = x_.BO + off;
-    g.o0 = Gm::OFF_O + orow(g.jf0) * OW + col;
-    g.sdst = x_.my_stream + (long long)(t4 - 31) * K * 2;
-    return g;
+__device__ __forceinline__ float ldsb(unsigned off) {
+    return *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sweep_sm4) + off);
+}
+__device__ __forceinline__ void stsb(unsigned off, float v) {
+    *reinterpret_cast<float*>(reinterpret_cast<char*>(sweep_sm4) + off) = v;
 }
 
-template <int K, bool G, int CK, bool Y = false, bool XL = false>
-__device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_, int tr,
-                                          const GroupAddr<K>* ga = nullptr, int gs = 0) {
-    using Gm = Geom<K, CK>;
-    constexpr int OW = Gm::OW;
-    const int lane = x_.lane, y0 = x_.y0, w = x_.w, h = x_.h;
-    const int c = (tr - lane - Gm::SH) & (Gm::RW - 1);
-    const int rc = x_.lb + c;
+// Step variants: X = 0 interior columns, 1 left border region (some x <= 0),
+// 2 right border region (some x >= w - 1), 3 both; YE: a band touching the
+// top or bottom row.  Without X and YE every pixel, flushed segment and stream
+// slot is inside the image: no clamps, no bounds checks.
+template <int K, int CK, int X, bool YE>
+__device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, int c4g, int t4, int s) {
+    using G = Geom<K, CK>;
+    constexpr bool XLm = X & 1, XRm = X & 2, XE = X != 0, BD = XE || YE;
+    const int lane = x_.lane;
+    const int t = t4 + s;
+    const float eps = x_.eps, omega = x_.omega;
+    // byte offset of ring row 2j, column (t - 2j + e)
+    auto C = [&](int e) { return x_.lb4 | (unsigned(c4g + 4 * (s + e)) & 124u); };
+    auto A = [&](int d) { return unsigned(4 * (G::OFF_A + (d - G::LA) * G::RW)); };
+    auto Ip = [&](int d) { return unsigned(4 * (G::OFF_I + (d - G::LI) * G::RW)); };
+    auto Fp = [&](int d) { return unsigned(4 * (G::OFF_F + d * G::RW)); };
+    auto Bp = [&](int d) { return unsigned(4 * (G::OFF_B + d * G::RW)); };
 
-    float2 recv[K];
+    // values from the row above row 2j: shfl.up of row 2j+1, lane 0 from the chunk
+    float2 rv[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        recv[k].x = __shfl_up_sync(kFull, st.outp[k].x, 1);
-        recv[k].y = __shfl_up_sync(kFull, st.outp[k].y, 1);
+        rv[k].x = __shfl_up_sync(kFull, st.o[1][k].x, 1);
+        rv[k].y = __shfl_up_sync(kFull, st.o[1][k].y, 1);
     }
-    if (lane == 0 && x_.has_up && (!G || (tr >= 0 && tr < x_.Umax))) {
-        const int cn = Gm::OFF_C + (tr % CK) * K * 2;
+    if (lane == 0 && x_.has_up) {
+        const int cn = G::OFF_C + (t & (CK - 1)) * K * 2;
 #pragma unroll
-        for (int k = 0; k < K; ++k) recv[k] = make_float2(lds(cn + 2 * k), lds(cn + 2 * k + 1));
+        for (int k = 0; k < K; ++k) rv[k] = make_float2(lds(cn + 2 * k), lds(cn + 2 * k + 1));
     }
 
-    float2 nv[K];
-    const int xs0 = tr - lane;  // slot-0 column
+    // slot-0 loads: row 2j (x0 = t - 2j), row 2j+1 (x1 = x0 - 1)
+    const float aR0 = ldsb(C(1) + A(0)), aR1 = ldsb(C(0) + A(1));
+    const float I0 = ldsb(C(0) + Ip(0)), I1 = ldsb(C(-1) + Ip(1));
+    const float2 FR0 = make_float2(ldsb(C(1) + Fp(0)), ldsb(C(1) + Bp(0)));
+    const float2 FR1 = make_float2(ldsb(C(0) + Fp(1)), ldsb(C(0) + Bp(1)));
+    const float aU0 = ldsb(C(0) + A(-1));
+    const float aD1 = ldsb(C(-1) + A(2));
+    const float2 FD1 = make_float2(ldsb(C(-1) + Fp(2)), ldsb(C(-1) + Bp(2)));
+
+    const int x0 = t - 2 * lane;
+    const int w = x_.w;
+    auto top = [&](int i, int k) { return YE && ((x_.ytop >> (i * K + k)) & 1u); };
+    auto bot = [&](int i, int k) { return YE && ((x_.ybot >> (i * K + k)) & 1u); };
+    auto xlo = [&](int x) { return XLm && x <= 0; };
+    auto xhi = [&](int x) { return XRm && x >= w - 1; };
+
+    // slot-0 coefficients
+    const float a0 = st.aRp[0], a1 = st.aRp[1];
+    float dL0 = st.dRp[0], dL1 = st.dRp[1], dU1 = st.dDp;
+    float aR0c = aR0, aR1c = aR1, aU0c = aU0, aD0c = aR1, aD1c = aD1;
+    if (xlo(x0)) dL0 = eps;
+    if (xlo(x0 - 1)) dL1 = eps;
+    if (xhi(x0)) aR0c = a0;
+    if (xhi(x0 - 1)) aR1c = a1;
+    if (top(0, 0)) aU0c = a0;
+    if (bot(0, 0)) aD0c = a0;
+    if (top(1, 0)) dU1 = eps;
+    if (bot(1, 0)) aD1c = a1;
+    const float dR0 = edge_weight(a0, aR0c, eps, omega), dU0 = edge_weight(a0, aU0c, eps, omega);
+    const float dD0 = edge_weight(a0, aD0c, eps, omega), dR1 = edge_weight(a1, aR1c, eps, omega);
+    const float dD1 = edge_weight(a1, aD1c, eps, omega);
+    CoefR co[R][K];
+    co[0][0] = coef_w(a0, dL0, dR0, dU0, dD0, I0);
+    co[1][0] = coef_w(a1, dL1, dR1, dU1, dD1, I1);
+
+    // row 2j's slots k >= 1: pixel (x0 - k, band row 2j - k), recomputed (K = 2:
+    // three of its four alphas are this and the previous step's)
+    float dRr[K];
+#pragma unroll
+    for (int k = 1; k < K; ++k) {
+        float a, aR, aD;
+        if (K == 2) {
+            a = st.aU0p;
+            aR = aU0;
+            aD = st.a0p;
+        } else {
+            a = ldsb(C(-k) + A(-k));
+            aR = ldsb(C(-k + 1) + A(-k));
+            aD = ldsb(C(-k) + A(-k + 1));
+        }
+        float aU = ldsb(C(-k) + A(-k - 1));
+        const float I = ldsb(C(-k) + Ip(-k));
+        float dL = st.dRr[k];
+        if (xlo(x0 - k)) dL = eps;
+        if (xhi(x0 - k)) aR = a;
+        if (top(0, k)) aU = a;
+        if (bot(0, k)) aD = a;
+        const float dR = edge_weight(a, aR, eps, omega);
+        co[0][k] = coef_w(a, dL, dR, edge_weight(a, aU, eps, omega), edge_weight(a, aD, eps, omega), I);
+        dRr[k] = dR;
+        co[1][k] = st.cp2[k - 1];
+    }
+
+    // the updates
+    float2 nv[R][K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        float2 L = st.outp[k], U = recv[k], R, D;
-        if (k == 0) {
-            R = make_float2(lds(rc + ring<K>(Gm::OFF_F, 0, 1 + Gm::SH)), lds(rc + ring<K>(Gm::OFF_B, 0, 1 + Gm::SH)));
-            D = make_float2(lds(rc + ring<K>(Gm::OFF_F, 1, Gm::SH)), lds(rc + ring<K>(Gm::OFF_B, 1, Gm::SH)));
-#ifdef FGM_N1_PROBE
-            // Cost probe of an in-sweep F/B upsample ("N1"): per step each
-            // lane gathers the 4 taps of F and B of its R pixel from a previous-level
-            // ring, reads an x-tap weight, interpolates (bilerp2), shuffles the result
-            // down as the upper lane's D, and lane 31 interpolates its own D from a
-            // second row pair.  Results are unchanged (added times a runtime zero).
-            {
-                const float tx = lds(rc + ring<K>(Gm::OFF_A, K, Gm::SH + 1));
-                const float2 a0 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 0, Gm::SH)), lds(rc + ring<K>(Gm::OFF_B, 0, Gm::SH)));
-                const float2 a1 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 0, Gm::SH + 2)), lds(rc + ring<K>(Gm::OFF_B, 0, Gm::SH + 2)));
-                const float2 c0 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 1, Gm::SH + 1)), lds(rc + ring<K>(Gm::OFF_B, 1, Gm::SH + 1)));
-                const float2 c1 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 1, Gm::SH + 2)), lds(rc + ring<K>(Gm::OFF_B, 1, Gm::SH + 2)));
-                const float2 v = bilerp2(a0, a1, c0, c1, tx, x_.probe_ty);
-                float2 dv;
-                dv.x = __shfl_down_sync(kFull, v.x, 1);
-                dv.y = __shfl_down_sync(kFull, v.y, 1);
-                if (lane == 31) {
-                    const float2 e0 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 2, Gm::SH)), lds(rc + ring<K>(Gm::OFF_B, 2, Gm::SH)));
-                    const float2 e1 = make_float2(lds(rc + ring<K>(Gm::OFF_F, 2, Gm::SH + 1)), lds(rc + ring<K>(Gm::OFF_B, 2, Gm::SH + 1)));
-                    dv = bilerp2(c0, c1, e0, e1, tx, x_.probe_ty);
-                }
-                R.x = fmaf(x_.probe_zero, v.x, R.x);
-                R.y = fmaf(x_.probe_zero, v.y, R.y);
-                D.x = fmaf(x_.probe_zero, dv.x, D.x);
-                D.y = fmaf(x_.probe_zero, dv.y, D.y);
+        {  // row 2j
+            float2 L = st.o[0][k], U = rv[k];
+            float2 Rn = k ? rv[k > 0 ? k - 1 : 0] : FR0;
+            float2 D = k ? st.o[0][k > 0 ? k - 1 : 0] : FR1;
+            if (BD) {
+                const float2 self = k ? st.rvp[k > 0 ? k - 1 : 0] : st.FRp[0];
+                if (xlo(x0 - k)) L = self;
+                if (xhi(x0 - k)) Rn = self;
+                if (top(0, k)) U = self;
+                if (bot(0, k)) D = self;
             }
-#endif
-        } else {
-            R = recv[k - 1];
-            D = st.outp[k - 1];
+            nv[0][k] = pixel_applyr(co[0][k], L, Rn, U, D);
         }
-        if (G || Y || XL) {
-            const int x = xs0 - k, y = y0 + lane - k;
-            const float2 self = k == 0 ? make_float2(lds(rc + ring<K>(Gm::OFF_F, 0, Gm::SH)),
-                                                     lds(rc + ring<K>(Gm::OFF_B, 0, Gm::SH)))
-                                       : st.rprev[k > 0 ? k - 1 : 0];
-            if (G || XL) {
-                if (!(x > 0)) L = self;
+        {  // row 2j+1
+            float2 L = st.o[1][k], U = st.o[0][k];
+            float2 Rn = k ? st.o[0][k > 0 ? k - 1 : 0] : FR1;
+            float2 D = k ? st.o[1][k > 0 ? k - 1 : 0] : FD1;
+            if (BD) {
+                const float2 self = k ? st.o2[k > 0 ? k - 1 : 0] : st.FRp[1];
+                if (xlo(x0 - 1 - k)) L = self;
+                if (xhi(x0 - 1 - k)) Rn = self;
+                if (top(1, k)) U = self;
+                if (bot(1, k)) D = self;
             }
-            if (G) {
-                if (!(x < w - 1)) R = self;
-            }
-            if (G || Y) {
-                if (!(y > 0)) U = self;
-                if (!(y < h - 1)) D = self;
-            }
-        }
-        nv[k] = apply_coef(st.co[k], L, R, U, D);
-    }
-
-    // coefficients of the next step's pixels; dL = this step's dR of the slot
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-        st.co[k] = next_coef<K, G, Y, XL>(rc, k, st.co[k].dR, xs0 + 1 - k, y0 + lane - k, w, h, x_.eps, x_.omega);
-
-    // output ring (last sweep only): column x & 15 == c & 15
-    {
-        bool ok = true;
-        if (G) {
-            const int x = xs0 - (K - 1);
-            ok = x >= 0 && x < w && y0 + lane - (K - 1) >= 0 && y0 + lane - (K - 1) < h;
-        }
-        if (ok) {  // (Y: rows outside the image land in the ring but are never flushed)
-            const int o = x_.ob + (c & (OW - 1));
-            sts(o, nv[K - 1].x);
-            sts(o + Gm::OPL, nv[K - 1].y);
+            nv[1][k] = pixel_applyr(co[1][k], L, Rn, U, D);
         }
     }
 
-    // boundary stream for the band below: lane 31's K outputs of this step
-    if (x_.has_down && lane == kBandRows - 1 && (!(G || XL) || (tr - 31 >= 0 && tr - 31 < x_.Umax))) {
-        float* dst = (!G && group_addr_ok<K>() && ga) ? ga->sdst + gs * K * 2 : x_.my_stream + size_t(tr - 31) * K * 2;
-        if (K % 2 == 0) {  // 16-byte aligned: u * 2K floats with K even
+    // output ring (last sweep only), row orow(2j + i), column x & 15.  Pixels
+    // outside the image land in slots that are rewritten or never flushed.
 #pragma unroll
-            for (int k = 0; k + 1 < K; k += 2)
-                st_relaxed_v4(dst + 2 * k, make_float4(nv[k].x, nv[k].y, nv[k + 1].x, nv[k + 1].y));
-        } else {
+    for (int i = 0; i < R; ++i) {
+        const unsigned o = (x_.ob4 + 64u * i) | (unsigned(c4g + 4 * (s - i - (K - 1))) & 60u);
+        stsb(o, nv[i][K - 1].x);
+        stsb(o + 4 * G::OPL, nv[i][K - 1].y);
+    }
+
+    // boundary stream for the band below: the last row's K outputs
+    if (x_.has_down && lane == 31) {
+        const int u = t - (BR - 1);
+        if ((!XLm || u >= 0) && (!XRm || u < x_.Umax)) {
+            float* dst = x_.my_stream + size_t(u) * K * 2;
+            if (K % 2 == 0) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) st_relaxed_v2(dst + 2 * k, nv[k]);
+                for (int k = 0; k + 1 < K; k += 2)
+                    st_relaxed_v4(dst + 2 * k, make_float4(nv[1][k].x, nv[1][k].y, nv[1][k + 1].x, nv[1][k + 1].y));
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; ++k) st_relaxed_v2(dst + 2 * k, nv[1][k]);
+            }
         }
     }
 
     __syncwarp();
-    // flush completed 16-column output row segments: rows jf (lanes 0-15) and
-    // jf+16 (lanes 16-31), one coalesced 64-byte store per plane each.
-    // Offsets are 32-bit, relative to the band's first output row.
-    if (!G && group_addr_ok<K>() && ga) {
-        bool ok = true;
-        if (Y) {
-            const int yf = y0 + ga->jf0 + gs - (K - 1);
-            ok = yf >= 0 && yf < h;
-        }
-        if (XL) ok = ok && ga->seg_ok;
-        if (ok) {
-            const long long ro = (long long)gs * x_.opitch;
-            const int o = ga->o0 + gs * OW;
-            stg(ga->fo + ro, lds(o));
-            stg(ga->bo + ro, lds(o + Gm::OPL));
-        }
-    } else {
-        const int col = lane & (OW - 1);
-        const int u = tr - (K - 1) - (OW - 1);
-        const int jf = (u & (OW - 1)) + (lane & 16);
-        const int xs = (u & ~(OW - 1)) - (lane & 16);  // segment start column (xf - 15)
-        bool ok = true;
-        if (G) {
-            const int yf = y0 + jf - (K - 1);
-            ok = xs >= 0 && xs + OW - 1 < w && yf >= 0 && yf < h;
-        } else {
-            if (Y) {
-                const int yf = y0 + jf - (K - 1);
-                ok = yf >= 0 && yf < h;
+    // flush the 16-column output row segments completed by this step: rows
+    // r = rho + 16 beta (beta = 0..3), lanes 0-15 / 16-31 two rows per store;
+    // column x = t - K - 14 - r + (lane & 15)
+    {
+        const int rho = (t - K - 14) & 15;
+        const unsigned lo = x_.flb4 + 64u * unsigned(rho);
+        const int off0 = rho * x_.op1 + t;
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
+            bool ok = true;
+            if (XE || YE) {
+                const int r = rho + 16 * (2 * hb + (lane >> 4));
+                const int x = t - K - 14 - r + (lane & 15);
+                if (XLm) ok = ok && x - (lane & 15) >= 0;
+                if (XRm) ok = ok && x < w;
+                if (YE) ok = ok && unsigned(x_.y0 + r - (K - 1)) < unsigned(x_.h);
             }
-            if (XL) ok = ok && xs >= 0;
+            if (ok) {
+                const int off = off0 + hb * 32 * x_.op1;
+                stg(x_.gF + off, ldsb(lo + hb * 34u * 64u));
+                stg(x_.gB + off, ldsb(lo + hb * 34u * 64u + 4u * G::OPL));
+            }
         }
-        if (ok) {  // off >= 0 here: unsigned, one IMAD.WIDE.U32 per plane
-            const unsigned off = unsigned(jf * x_.opitch + xs + col);
-            const int o = Gm::OFF_O + orow(jf) * OW + col;
-            stg(x_.FO + off, lds(o));
-            stg(x_.BO + off, lds(o + Gm::OPL));
-        }
-        if (G && ((w - 1) & (OW - 1)) != OW - 1) {  // partial last segment of a row
-            const int je = tr - (K - 1) - (w - 1);
-            const int x0 = (w - 1) & ~(OW - 1);
-            const int ye = y0 + je - (K - 1);
-            if (je >= 0 && je < 32 && ye >= 0 && ye < h && lane < w - x0) {
-                const unsigned off = unsigned(je * x_.opitch + x0 + lane);
-                const int o = Gm::OFF_O + orow(je) * OW + lane;
-                stg(x_.FO + off, lds(o));
-                stg(x_.BO + off, lds(o + Gm::OPL));
+        if (XRm && ((w - 1) & (G::OW - 1)) != G::OW - 1) {  // the partial last segment of a row
+            const int re = t - (K - 1) - (w - 1);
+            const int xb = (w - 1) & ~(G::OW - 1);
+            const int y = x_.y0 + re - (K - 1);
+            if (re >= 0 && re < BR && y >= 0 && y < x_.h && lane < w - xb) {
+                // (lanes < 16: gF = FO + lane - K - 14)
+                const int off = re * (x_.op1 + 1) + xb + K + 14;
+                const unsigned o = unsigned(4 * (G::OFF_O + orow(re) * G::OW + lane));
+                stg(x_.gF + off, ldsb(o));
+                stg(x_.gB + off, ldsb(o + 4u * G::OPL));
             }
         }
     }
 
+    // carry
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        if (G || Y || XL) st.rprev[k] = recv[k];
-        st.outp[k] = nv[k];
+        st.o2[k] = st.o[0][k];
+        st.rvp[k] = rv[k];
+        st.o[0][k] = nv[0][k];
+        st.o[1][k] = nv[1][k];
+        st.cp2[k] = st.cp1[k];
+        st.cp1[k] = co[0][k];
+        if (k >= 1) st.dRr[k] = dRr[k];
+    }
+    st.aU0p = aU0;
+    st.a0p = a0;
+    st.FRp[0] = FR0;
+    st.FRp[1] = FR1;
+    st.aRp[0] = aR0;
+    st.aRp[1] = aR1;
+    st.dRp[0] = dR0;
+    st.dRp[1] = dR1;
+    st.dDp = dD0;
+}
+
+// ---- ring refills -----------------------------------------------------------
+// Plane p (0 alpha, 1 image, 2 F, 3 B) of band row r: segment n (columns
+// 16n .. 16n+15) is issued at step 16(n-1) + r - M_p + phase(M_p), when the
+// segment n-2 in its ring slot has left the read window.  In the group of
+// steps [t4, t4+4) that is Z = t4 + M_p - phase(M_p) (a multiple of 4): rows
+// r = 16 beta + (Z & 15) + rho (rho = 0..3) get segment n = (Z >> 4) + 1 - beta.
+struct RefillSrc {
+    const float* base[4];  // plane row 0 (image row y0), column 0
+    int pitch[4];
+};
+
+template <int K, int CK>
+__device__ __forceinline__ constexpr int plane_lo(int p) {
+    using G = Geom<K, CK>;
+    return p == 0 ? G::LA : p == 1 ? G::LI : 0;
+}
+__device__ __forceinline__ constexpr int plane_hi(int p) { return p == 1 ? BR - 1 : BR; }
+template <int K, int CK>
+__device__ __forceinline__ constexpr int plane_off(int p) {
+    using G = Geom<K, CK>;
+    return p == 0 ? G::OFF_A : p == 1 ? G::OFF_I : p == 2 ? G::OFF_F : G::OFF_B;
+}
+template <int K, int CK>
+__device__ __forceinline__ constexpr int plane_m(int p) {
+    using G = Geom<K, CK>;
+    return p == 0 ? G::MA : p == 1 ? G::MI : G::MF;
+}
+template <int K, int CK>
+__device__ __forceinline__ constexpr int plane_rows(int p) {
+    using G = Geom<K, CK>;
+    return p == 0 ? G::NA : p == 1 ? G::NI : G::NF;
+}
+
+// One 16-byte piece (4 columns from c) of plane P, band row r, with every check.
+template <int K, bool V4, int CK, int P>
+__device__ __forceinline__ void put_piece(const RefillSrc& S, unsigned sbase, int r, int c, int y0, int w, int h) {
+    using G = Geom<K, CK>;
+    if (r < plane_lo<K, CK>(P) || r > plane_hi(P) || c < 0 || c >= w) return;
+    const int y = y0 + r;
+    if (y < 0 || y >= h) return;
+    const float* g = S.base[P] + (long long)r * S.pitch[P] + c;
+    const unsigned d = sbase + 4u * unsigned(plane_off<K, CK>(P) + (r - plane_lo<K, CK>(P)) * G::RW + (c & (G::RW - 1)));
+    const int nb = min(w - c, 4);
+    if (V4) {
+        cp_async16(d, g, nb * 4);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cp_async4(d + 4 * i, i < nb ? g + i : g, i < nb ? 4 : 0);
     }
 }
 
+// The refills of plane P in group t4, every piece checked (band edges, image
+// edges, jobs without 16-byte aligned rows).
+template <int K, bool V4, int CK, int P>
+__device__ __forceinline__ void refill_checked_p(const RefillSrc& S, unsigned sbase, int t4, int lane, int y0, int w,
+                                                 int h) {
+    using G = Geom<K, CK>;
+    const int q = lane & 3, rho = (lane >> 2) & 3, bl = lane >> 4;
+    constexpr int m = plane_m<K, CK>(P);
+    const int Z = t4 + m - G::phase(m);
+    const int zr = Z & 15, zh = Z >> 4;
+    // beta = -1 .. 4 covers band rows -16 .. 79
+#pragma unroll
+    for (int b0 = -1; b0 <= 3; b0 += 2) {
+        const int beta = b0 + bl;
+        const int r = 16 * beta + zr + rho;
+        const int c0 = 16 * (zh + 1 - beta);
+        if (c0 >= 32) put_piece<K, V4, CK, P>(S, sbase, r, c0 + 4 * q, y0, w, h);
+    }
+}
+template <int K, bool V4, int CK>
+__device__ __forceinline__ void refill_checked(const RefillSrc& S, unsigned sbase, int t4, int lane, int y0, int w,
+                                               int h) {
+    refill_checked_p<K, V4, CK, 0>(S, sbase, t4, lane, y0, w, h);
+    refill_checked_p<K, V4, CK, 1>(S, sbase, t4, lane, y0, w, h);
+    refill_checked_p<K, V4, CK, 2>(S, sbase, t4, lane, y0, w, h);
+    refill_checked_p<K, V4, CK, 3>(S, sbase, t4, lane, y0, w, h);
+}
+
+// Interior groups of interior bands: every piece of the 4 x 4 main row blocks
+// (band rows 0..63) is inside the image and the job's rows are 16-byte
+// aligned; the extra rows (alpha -K..-1 and 64, image -(K-1)..-1, F/B 64) are
+// refilled in the groups whose phase reaches them.
+template <int K, int CK, int P>
+__device__ __forceinline__ void refill_fast_p(const RefillSrc& S, const float* gl, unsigned ss, int t4, int lane,
+                                              unsigned sbase, int y0, int w, int h) {
+    using G = Geom<K, CK>;
+    const int bl = lane >> 4;
+    constexpr int m = plane_m<K, CK>(P);
+    const int Z = t4 + m - G::phase(m);
+    const int zr = Z & 15, zh = Z >> 4;
+    const float* g = gl + ((long long)zr * S.pitch[P] + 16 * zh);
+    const unsigned d = ss + 4u * unsigned(plane_off<K, CK>(P) - plane_lo<K, CK>(P) * G::RW) +
+                       unsigned(zr * G::RW * 4 + 64 * ((zh + 1 + bl) & 1));
+    cp_async16f(d, g);
+    cp_async16f(d + 4u * 32u * G::RW, g + 32LL * S.pitch[P] - 32);
+    // extra rows above row 0 (beta = -1) and row 64 (beta = 4)
+    if (P <= 1 && zr == 12) {
+        const int rho = (lane >> 2) & 3, q = lane & 3;
+        if (bl == 0) put_piece<K, true, CK, P>(S, sbase, -4 + rho, 16 * (zh + 2) + 4 * q, y0, w, h);
+    }
+    if (P != 1 && zr == 0) {
+        if (lane < 4) put_piece<K, true, CK, P>(S, sbase, BR, 16 * (zh - 3) + 4 * (lane & 3), y0, w, h);
+    }
+}
+
+// Prologue: segments 0 and 1 of every ring row of plane P.
+template <int K, bool V4, int CK, int P>
+__device__ __forceinline__ void refill_prologue_p(const RefillSrc& S, unsigned sbase, int lane, int y0, int w, int h) {
+    constexpr int N = plane_rows<K, CK>(P) * 8;  // 8 pieces per row: columns 0..31
+    for (int it = lane; it < N; it += 32)
+        put_piece<K, V4, CK, P>(S, sbase, (it >> 3) + plane_lo<K, CK>(P), 4 * (it & 7), y0, w, h);
+}
+template <int K, bool V4, int CK>
+__device__ __forceinline__ void refill_prologue(const RefillSrc& S, unsigned sbase, int lane, int y0, int w, int h) {
+    refill_prologue_p<K, V4, CK, 0>(S, sbase, lane, y0, w, h);
+    refill_prologue_p<K, V4, CK, 1>(S, sbase, lane, y0, w, h);
+    refill_prologue_p<K, V4, CK, 2>(S, sbase, lane, y0, w, h);
+    refill_prologue_p<K, V4, CK, 3>(S, sbase, lane, y0, w, h);
+}
+
+// ---- boundary-stream chunks ---------------------------------------------------
 template <int K, int CK>
 __device__ __forceinline__ bool chunk_complete(float4 q, int u0, int Umax, int lane) {
     using G = Geom<K, CK>;
@@ -666,9 +533,6 @@ __device__ __forceinline__ bool chunk_complete(float4 q, int u0, int Umax, int l
              (b + 3 < nvalid && is_sentinel(q.w)));
 }
 
-// Poll chunk `u0 / CK` of the band above until every word of it is
-// written; leaves it in the chunk buffer.  `v` holds a load issued earlier
-// and is re-polled only while incomplete.
 // The launch-wide failure state of a sweep: a per-launch abort flag (zeroed
 // with the ticket) and a persistent per-device fault counter.
 struct SweepFail {
@@ -683,27 +547,22 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-// Poll chunk `u0 / CK` of the band above until every word of it is
-// written; leaves it in the chunk buffer.  `v` holds a load issued earlier
-// and is re-polled only while incomplete.  Bounded (SURVEY.md section 5,
-// "timeout -> error, not a hang"): after spin_ns the wait raises the launch's
-// abort flag, counts a device fault and returns false; every other waiter of
-// the launch then gives up at once.
+// Poll chunk `u0 / CK` of the band above until every word of it is written;
+// leaves it in the chunk buffer.  `v` holds a load issued earlier and is
+// re-polled only while incomplete.  Bounded: after spin_ns the wait raises the
+// launch's abort flag, counts a device fault and returns false; every other
+// waiter of the launch then gives up at once.
 template <int K, int CK>
 __device__ __forceinline__ bool acquire_chunk(float4 v, const float* up_stream, int u0, int Umax, int lane,
-                                              int chunk, const SweepFail& F) {
+                                              const SweepFail& F) {
     using G = Geom<K, CK>;
-    const int nvalid = min(CK, Umax - u0) * K * 2;  // floats
+    const int nvalid = min(CK, Umax - u0) * K * 2;
     const bool mine = lane < G::CH4 && 4 * lane < nvalid;
-    // (exponential back-off up to 4 us was measured: no effect on batches,
-    // slower single images)
-    // (the abort flag and the clock are checked every 256 polls only: a
-    // check in every poll slows the hand-over of latency-bound launches)
     unsigned long long t0 = 0;
     for (unsigned n = 0; !__all_sync(kFull, chunk_complete<K, CK>(v, u0, Umax, lane)); ++n) {
         __nanosleep(32);
         if (mine) v = ld_relaxed_v4(up_stream + size_t(u0) * K * 2 + 4 * lane);
-        if ((n & 255u) == 255u) {
+        if ((n & 255u) == 255u) {  // the abort flag and the clock every 256 polls
             int ab = 0;
             if (lane == 0) {
                 const unsigned long long now = global_ns();
@@ -718,172 +577,152 @@ __device__ __forceinline__ bool acquire_chunk(float4 v, const float* up_stream, 
             if (__shfl_sync(kFull, ab, 0)) return false;
         }
     }
-    if (mine) sts4(chunk + 4 * lane, v);
+    if (mine) sts4(G::OFF_C + 4 * lane, v);
     return true;
 }
 
-#ifdef FGM_TRACE
-__device__ unsigned long long g_trace[4 * 65536];  // per item: start, first chunk, fast phase, end (ns)
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#endif
-
-#ifndef FGM_REPOLL
-#define FGM_REPOLL 1
-#endif
 template <int K, bool V4, int CK>
 __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int lane, unsigned sbase, float eps,
                                          float omega, const SweepFail& F, int fault) {
-#ifdef FGM_TRACE
-    const int titem = (J.band_base + q) * 3 + ch;
-    if (lane == 0 && titem < 65536) g_trace[4 * titem] = gtimer();
-#endif
-    using Gm = Geom<K, CK>;
+    using G = Geom<K, CK>;
     const int w = J.w, h = J.h;
-    const int y0 = q * kBandRows;
+    const int y0 = q * BR;
     const int Umax = w + K - 1;
     const size_t slen = sweep_stream_len(w, K);
-    const int sid = q * 3 + ch;  // stream index of this (band, channel)
+    const int sid = q * 3 + ch;
     const float* up_stream = q > 0 ? J.stream + size_t(sid - 3) * slen : nullptr;
 
-    StepCtx<K> cx;
-    cx.lb = lane * Gm::RS;
-    cx.ob = Gm::OFF_O + orow(lane) * Gm::OW;
+    StepCtx cx;
     cx.lane = lane;
     cx.y0 = y0;
     cx.w = w;
     cx.h = h;
+    cx.Umax = Umax;
+    cx.lb4 = 256u * unsigned(lane);
+    cx.ob4 = unsigned(4 * (G::OFF_O + orow(2 * lane) * G::OW));
+    cx.flb4 = unsigned(4 * (G::OFF_O + 17 * (lane >> 4) * G::OW + (lane & 15)));
     cx.has_up = q > 0;
     cx.has_down = q < J.nb - 1 && !(fault == 1 && q == 0);  // (fault 1: band 0 never publishes)
-    cx.Umax = Umax;
     cx.my_stream = J.stream + size_t(sid) * slen;
-    // band-relative output base (row y0 - (K-1) may be -1.. for the first
-    // band: only the pointer arithmetic goes there, stores are bounds-checked)
-    cx.FO = J.fg_out + (long long)ch * J.ostride + (long long)(y0 - (K - 1)) * J.opitch;
-    cx.BO = J.bg_out + (long long)ch * J.ostride + (long long)(y0 - (K - 1)) * J.opitch;
-    cx.opitch = J.opitch;
+    {
+        const long long fo = (long long)(y0 - (K - 1)) * J.opitch + 16LL * (lane >> 4) * (J.opitch - 1) +
+                             (lane & 15) - K - 14;
+        cx.gF = J.fg_out + (long long)ch * J.ostride + fo;
+        cx.gB = J.bg_out + (long long)ch * J.ostride + fo;
+    }
+    cx.op1 = J.opitch - 1;
+    cx.ytop = cx.ybot = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int y = y0 + 2 * lane + i - k;
+            if (y <= 0) cx.ytop |= 1u << (i * K + k);
+            if (y >= h - 1) cx.ybot |= 1u << (i * K + k);
+        }
     cx.eps = eps;
     cx.omega = omega;
-#ifdef FGM_N1_PROBE
-    cx.probe_zero = eps * 0.0f;
-    cx.probe_ty = 0.25f + 0.01f * float(lane);
-#endif
 
-    // rows this lane streams
-    const RowSrc own = make_rowsrc<K>(J, ch, y0, lane, true, true, true, sbase);
-    const bool has_x = lane >= 32 - K || lane == 0;
-    const RowSrc ext =
-        make_rowsrc<K>(J, ch, y0, lane == 0 ? 32 : lane - 32, has_x, lane >= 33 - K, lane == 0, sbase);
-#ifndef FGM_FLAT_ISSUE
-#define FGM_FLAT_ISSUE 1
-#endif
-#if FGM_FLAT_ISSUE
-    const FlatSrc<K> flat = make_flat<K, CK>(J, ch, y0, lane, sbase);
-#endif
+    RefillSrc S;
+    S.base[0] = J.alpha + (long long)y0 * J.ipitch;
+    S.base[1] = J.img + (long long)ch * J.istride + (long long)y0 * J.ipitch;
+    S.base[2] = J.fg_in + (long long)ch * J.fstride + (long long)y0 * J.fpitch;
+    S.base[3] = J.bg_in + (long long)ch * J.fstride + (long long)y0 * J.fpitch;
+    S.pitch[0] = S.pitch[1] = J.ipitch;
+    S.pitch[2] = S.pitch[3] = J.fpitch;
+    // this lane's piece of the main refill blocks: rows 16*bl + rho (+ (Z & 15),
+    // + 32 for the second instruction), columns 16 (1 - bl) + 4 q (+ 16 (Z >> 4))
+    const int bl = lane >> 4, rho = (lane >> 2) & 3, qq = lane & 3;
+    const long long lo0 = 16 * (1 - bl) + 4 * qq;
+    const float* glA = S.base[0] + (long long)(16 * bl + rho) * S.pitch[0] + lo0;
+    const float* glI = S.base[1] + (long long)(16 * bl + rho) * S.pitch[1] + lo0;
+    const float* glF = S.base[2] + (long long)(16 * bl + rho) * S.pitch[2] + lo0;
+    const float* glB = S.base[3] + (long long)(16 * bl + rho) * S.pitch[3] + lo0;
+    const unsigned ss = sbase + 4u * unsigned((16 * bl + rho) * G::RW + 4 * qq);
+
+    refill_prologue<K, V4, CK>(S, sbase, lane, y0, w, h);
+    cp_commit();
+    cp_commit();  // (an empty group: the first wait_group<1> covers the prologue)
 
     LaneState<K> st;
 #pragma unroll
-    for (int k = 0; k < K; ++k) st.outp[k] = st.rprev[k] = make_float2(0.0f, 0.0f);
+    for (int k = 0; k < K; ++k) {
+        st.o[0][k] = st.o[1][k] = st.o2[k] = st.rvp[k] = make_float2(0.0f, 0.0f);
+        st.cp1[k] = st.cp2[k] = coef_w(0.5f, 1.0f, 1.0f, 1.0f, 1.0f, 0.0f);
+        st.dRr[k] = eps;
+    }
+    st.aRp[0] = st.aRp[1] = st.aU0p = st.a0p = 0.0f;
+    st.FRp[0] = st.FRp[1] = make_float2(0.0f, 0.0f);
+    st.dRp[0] = st.dRp[1] = st.dDp = eps;
 
-    // prologue: the loads "issued before" the first group, then M-1 empty
-    // groups so that every group waits with the same cp.async.wait_group M-1
-    constexpr int S = Gm::S;
-    constexpr int t0 = -S;
-    prologue_row<K, V4, CK>(own, t0, w);
-    if (has_x) prologue_row<K, V4, CK>(ext, t0, w);
-    cp_commit();
-#pragma unroll
-    for (int i = 1; i < Gm::M; ++i) cp_commit();
-    // the band above's first chunk, polled when needed
     float4 pend = make_float4(0.f, 0.f, 0.f, 0.f);
-    const bool lane_ch = lane < Gm::CH4;
+    const bool lane_ch = lane < G::CH4;
     bool pend_ok = false;  // pend holds the complete next chunk
     if (cx.has_up && lane_ch) pend = ld_relaxed_v4(up_stream + 4 * lane);
 
-    // Border groups: bands touching row 0 or h-1, else the first and last ~32
-    // steps.  Fast groups need no neighbour clamping and no bounds checks.
-    const bool yband = y0 - (K - 1) <= 0 || y0 + 31 >= h - 1;
-    const int fast_lo = 32 + K, fast_hi = w - 2;  // a step tr is fast iff fast_lo <= tr < fast_hi
-    const int tend = 31 + Umax;                   // lane 31's last column is Umax-1
-    // groups whose issued blocks are inside [0, w) for every row -K .. 32
-    const int issue_lo = 32 - Gm::L, issue_hi = w - 2 * S - Gm::L - K;
-    for (int t4 = t0; t4 < tend; t4 += S) {
-        cp_wait<Gm::M - 1>();
+    const bool yband = y0 - (K - 1) <= 0 || y0 + BR - 1 >= h - 1;
+    // Steps t4..t4+3 have every pixel at 1 <= x <= w - 2, every flushed
+    // segment at x >= 0 and every stream slot in range iff
+    // t4 >= fast_lo (t4 - 63 - (K-1) >= 1 and t4 - K - 14 - 63 >= 0) and
+    // t4 + 3 <= fast_hi.  Left-region groups (t4 < fast_lo) need no right
+    // checks when fast_lo + 3 <= fast_hi.
+    const int fast_lo = (78 + K + 3) & ~3, fast_hi = w - 2;
+    const bool split = fast_lo + 3 <= fast_hi;
+    // refills of groups t4 in [rf_lo, rf_hi) are inside rows 0..63 and [32, w)
+    const bool rf_band = J.vec4 && y0 >= K && y0 + BR < h;
+    const int rf_lo = 72 + 2 * K, rf_hi = w - 32;
+    const int tend = Umax + BR - 1;  // steps t < tend
+    for (int t4 = -4; t4 < tend; t4 += 4) {
+        cp_wait<G::WAITN>();
         __syncwarp();
-        if (t4 < 0) {
-            // coefficients of step 0 (computed "at step -1")
-            const int rc = cx.lb + ((-1 - lane - Gm::SH) & (Gm::RW - 1));
-#pragma unroll
-            for (int k = 0; k < K; ++k) st.co[k] = first_coef<K>(rc, k, -lane - k, y0 + lane - k, w, h, eps, omega);
-        } else {
-            if (cx.has_up && t4 < Umax) {
-                const int nxt = (t4 & ~(CK - 1)) + CK;  // the next chunk's first column
-                if ((t4 % CK) == 0) {
-                    if (!acquire_chunk<K, CK>(pend, up_stream, t4, Umax, lane, Gm::OFF_C, F)) {
-                        cp_wait<0>();  // the launch is aborted: drop the band
-                        __syncwarp();
-                        return;
-                    }
-#ifdef FGM_TRACE
-                    if (t4 == 0 && lane == 0 && titem < 65536) g_trace[4 * titem + 1] = gtimer();
-                    if (t4 == 64 && lane == 0 && titem < 65536) g_trace[4 * titem + 2] = gtimer();
-#endif
-                    pend_ok = false;
-                    if (nxt < Umax && lane_ch)  // prefetch the next chunk
-                        pend = ld_relaxed_v4(up_stream + size_t(nxt) * K * 2 + 4 * lane);
-                } else if (FGM_REPOLL && !pend_ok && nxt < Umax) {
-                    // the prefetch found the next chunk incomplete: re-poll it
-                    // now rather than a full round trip when it is needed
-                    pend_ok = __all_sync(kFull, chunk_complete<K, CK>(pend, nxt, Umax, lane));
-                    if (!pend_ok && lane_ch) pend = ld_relaxed_v4(up_stream + size_t(nxt) * K * 2 + 4 * lane);
+        if (cx.has_up && t4 >= 0 && t4 < Umax) {
+            const int nxt = (t4 & ~(CK - 1)) + CK;  // the next chunk's first column
+            if ((t4 & (CK - 1)) == 0) {
+                if (!acquire_chunk<K, CK>(pend, up_stream, t4, Umax, lane, F)) {
+                    cp_wait<0>();  // the launch is aborted: drop the band
+                    __syncwarp();
+                    return;
                 }
+                pend_ok = false;
+                if (nxt < Umax && lane_ch) pend = ld_relaxed_v4(up_stream + size_t(nxt) * K * 2 + 4 * lane);
+            } else if (!pend_ok && nxt < Umax) {
+                // the prefetch found the next chunk incomplete: re-poll it now
+                pend_ok = __all_sync(kFull, chunk_complete<K, CK>(pend, nxt, Umax, lane));
+                if (!pend_ok && lane_ch) pend = ld_relaxed_v4(up_stream + size_t(nxt) * K * 2 + 4 * lane);
             }
             __syncwarp();
-            if (t4 >= fast_lo && t4 + S <= fast_hi && !yband) {
-                const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
-#pragma unroll
-                for (int s = 0; s < S; ++s) band_step<K, false, CK>(st, cx, t4 + s, &ga, s);
-            } else if (t4 >= fast_lo && t4 + S <= fast_hi) {
-                const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
-#pragma unroll
-                for (int s = 0; s < S; ++s) band_step<K, false, CK, true>(st, cx, t4 + s, &ga, s);
-            } else if (t4 < fast_lo && t4 + S <= fast_hi) {  // band start: left border only
-                if (yband) {
-                    const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
-#pragma unroll
-                    for (int s = 0; s < S; ++s) band_step<K, false, CK, true, true>(st, cx, t4 + s, &ga, s);
-                } else {
-                    const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
-#pragma unroll
-                    for (int s = 0; s < S; ++s) band_step<K, false, CK, false, true>(st, cx, t4 + s, &ga, s);
-                }
-            } else {
-#pragma unroll 1
-                for (int s = 0; s < S; ++s) band_step<K, true, CK>(st, cx, t4 + s);
-            }
         }
-        __syncwarp();  // every lane is done with the ring slots the next loads overwrite
-        if (V4 && !yband && t4 >= issue_lo && t4 < issue_hi) {
-#if FGM_FLAT_ISSUE
-            issue_flat<K, CK>(flat, t4);
-#else
-            issue_row_fast<K, 15u, CK>(own, t4);
-            issue_row_fast<K, 0u, CK>(ext, t4);
-#endif
+        const int c4g = 4 * t4 - 8 * lane;
+        const bool xl = t4 < fast_lo, xr = t4 + 3 > fast_hi;
+        if (!xl && !xr && !yband) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s) band_step<K, CK, 0, false>(st, cx, c4g, t4, s);
+        } else if (!xl && !xr) {
+#pragma unroll 1
+            for (int s = 0; s < 4; ++s) band_step<K, CK, 0, true>(st, cx, c4g, t4, s);
+        } else if (split && !xr) {
+#pragma unroll 1
+            for (int s = 0; s < 4; ++s) band_step<K, CK, 1, true>(st, cx, c4g, t4, s);
+        } else if (split && !xl) {
+#pragma unroll 1
+            for (int s = 0; s < 4; ++s) band_step<K, CK, 2, true>(st, cx, c4g, t4, s);
         } else {
-            issue_row<K, V4, CK>(own, t4, w);
-            if (has_x) issue_row<K, V4, CK>(ext, t4, w);
+#pragma unroll 1
+            for (int s = 0; s < 4; ++s) band_step<K, CK, 3, true>(st, cx, c4g, t4, s);
+        }
+        __syncwarp();  // every lane is done with the ring slots the refills overwrite
+        if (rf_band && t4 >= rf_lo && t4 < rf_hi) {
+            refill_fast_p<K, CK, 0>(S, glA, ss, t4, lane, sbase, y0, w, h);
+            refill_fast_p<K, CK, 1>(S, glI, ss, t4, lane, sbase, y0, w, h);
+            refill_fast_p<K, CK, 2>(S, glF, ss, t4, lane, sbase, y0, w, h);
+            refill_fast_p<K, CK, 3>(S, glB, ss, t4, lane, sbase, y0, w, h);
+        } else {
+            refill_checked<K, V4, CK>(S, sbase, t4, lane, y0, w, h);
         }
         cp_commit();
     }
     cp_wait<0>();
     __syncwarp();
-#ifdef FGM_TRACE
-    if (lane == 0 && titem < 65536) g_trace[4 * titem + 3] = gtimer();
-#endif
 }
 
 struct SweepArgs {
@@ -896,7 +735,7 @@ struct SweepArgs {
     int fault;  // debug fault injection (fgm_debug_fault)
 };
 
-template <int K, bool V4, int CK>
+template <int K, int CK>
 __global__ void __launch_bounds__(32, 1) sweep_kernel(SweepArgs A) {
     const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sweep_sm4));
     const int lane = threadIdx.x & 31;
@@ -907,11 +746,10 @@ __global__ void __launch_bounds__(32, 1) sweep_kernel(SweepArgs A) {
         if (tk >= unsigned(A.total) || *reinterpret_cast<volatile int*>(A.fail.abort_flag)) return;
         const int2 jb = A.order[tk];  // (job, band * 3 + channel)
         const SweepJob J = A.jobs[jb.x];
-        if (V4 && !J.vec4) {
+        if (J.vec4)
+            run_band<K, true, CK>(J, jb.y / 3, jb.y % 3, lane, sbase, A.eps, A.omega, A.fail, A.fault);
+        else
             run_band<K, false, CK>(J, jb.y / 3, jb.y % 3, lane, sbase, A.eps, A.omega, A.fail, A.fault);
-        } else {
-            run_band<K, V4, CK>(J, jb.y / 3, jb.y % 3, lane, sbase, A.eps, A.omega, A.fail, A.fault);
-        }
     }
 }
 
@@ -922,18 +760,18 @@ cudaError_t sweep_grid_cap(int& cap) {
     static PerDevice<int> cfg;
     return cfg.get(cap, [](int dev, int& v) {
         const int sm4 = int(Geom<K, 4>::TOTAL * sizeof(float)), sm16 = int(Geom<K, kChunk>::TOTAL * sizeof(float));
-        cudaError_t e = cudaFuncSetAttribute(sweep_kernel<K, true, kChunk>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm16);
+        cudaError_t e = cudaFuncSetAttribute(sweep_kernel<K, kChunk>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm16);
         // the largest shared-memory carveout: the rings, not L1, bound the resident warps
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(sweep_kernel<K, true, kChunk>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            e = cudaFuncSetAttribute(sweep_kernel<K, kChunk>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(sweep_kernel<K, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4);
+            e = cudaFuncSetAttribute(sweep_kernel<K, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(sweep_kernel<K, true, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            e = cudaFuncSetAttribute(sweep_kernel<K, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         int sms = 0, per_sm = 0;
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<K, true, kChunk>, 32, size_t(sm16));
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<K, kChunk>, 32, size_t(sm16));
         v = std::max(1, sms * std::max(1, per_sm));
         return e;
     });
@@ -941,8 +779,8 @@ cudaError_t sweep_grid_cap(int& cap) {
 
 // Launches whose (band, channel) items all fit on the GPU at once are
 // latency-bound single images: their critical path crosses every band, one
-// boundary-stream chunk per hand-over, so they poll 4-column chunks (a ~20%
-// shorter hand-over lag); throughput launches poll 16-column chunks.
+// boundary-stream chunk per hand-over, so they poll 4-column chunks (a shorter
+// hand-over lag); throughput launches poll 16-column chunks.
 template <int K>
 cudaError_t launch_sweep_k(const SweepArgs& A, cudaStream_t s) {
     int cap = 0;
@@ -950,9 +788,9 @@ cudaError_t launch_sweep_k(const SweepArgs& A, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(A.total, cap));
     if (A.total <= cap)
-        sweep_kernel<K, true, 4><<<grid, 32, size_t(Geom<K, 4>::TOTAL) * sizeof(float), s>>>(A);
+        sweep_kernel<K, 4><<<grid, 32, size_t(Geom<K, 4>::TOTAL) * sizeof(float), s>>>(A);
     else
-        sweep_kernel<K, true, kChunk><<<grid, 32, size_t(Geom<K, kChunk>::TOTAL) * sizeof(float), s>>>(A);
+        sweep_kernel<K, kChunk><<<grid, 32, size_t(Geom<K, kChunk>::TOTAL) * sizeof(float), s>>>(A);
     return cudaGetLastError();
 }
 
@@ -967,20 +805,14 @@ __global__ void stream_fill_kernel(const SweepJob* __restrict__ jobs, int K) {
 
 }  // namespace
 
-cudaError_t launch_stream_fill(const SweepJob* jobs_dev, int njobs, int K, size_t max_floats, cudaStream_t s) {
+cudaError_t launch_stream_fill(const SweepJob* jobs, int njobs, int K, size_t max_floats, cudaStream_t s) {
     if (njobs <= 0) return cudaSuccess;
     const int gx = int(std::min<size_t>(std::max<size_t>((max_floats / 4 + 255) / 256, 1), 64));
-    stream_fill_kernel<<<dim3(gx, njobs), 256, 0, s>>>(jobs_dev, K);
+    stream_fill_kernel<<<dim3(gx, njobs), 256, 0, s>>>(jobs, K);
     return cudaGetLastError();
 }
 
 int sweep_supported_k(int K) { return K >= 1 && K <= 4; }
-
-#ifdef FGM_TRACE
-extern "C" int fgm_debug_trace(unsigned long long* out, int n) {
-    return int(cudaMemcpyFromSymbol(out, g_trace, size_t(n) * sizeof(unsigned long long)));
-}
-#endif
 
 size_t sweep_smem_bytes(int K) {
     switch (K) {

@@ -75,11 +75,14 @@ def test_ml_vs_oracle_params(fgm, cuda, orc, oracle_mod, kw):
     assert_close("bg", b, ob)
 
 
-@pytest.mark.parametrize("w,h", [(7, 100), (37, 65), (39, 200), (40, 33), (41, 31), (64, 97), (300, 32), (300, 33)])
-def test_sweep_border_modes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h):
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("w,h", [(7, 100), (37, 65), (39, 200), (40, 33), (41, 31), (64, 97), (300, 32), (300, 33),
+                                 (90, 130), (200, 129), (123, 64), (96, 66)])
+def test_sweep_border_modes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, kernel):
     # narrow levels and bands at the row borders: the border / row-border /
-    # band-start variants of K3 (sweep.cu) against the fp64 oracle, level by
-    # level through the single-level entry (BASELINE params, K = 1..4)
+    # band-start variants of both K3 kernels (sweep_lat.cu: 1, sweep.cu: 2)
+    # against the fp64 oracle, level by level through the single-level entry
+    # (BASELINE params, K = 1..4)
     rng = np.random.default_rng(w * 1000 + h)
     img = rng.random((3, h, w)).astype(np.float32)
     a = rng.random((h, w)).astype(np.float32)
@@ -90,7 +93,7 @@ def test_sweep_border_modes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h):
         of, ob = orc.sweep(img.astype(np.float64), a.astype(np.float64), f0.astype(np.float64),
                            b0.astype(np.float64), p, K)
         gf, gb = fgm.sweep_passes_cuda(dev(img, cuda), dev(a, cuda), dev(f0, cuda), dev(b0, cuda), K, p.eps_r,
-                                       p.omega)
+                                       p.omega, kernel)
         torch.cuda.synchronize()
         assert_close("fg", gf.double().cpu().numpy(), of, tol_max=2e-5, tol_mean=1e-6)
         assert_close("bg", gb.double().cpu().numpy(), ob, tol_max=2e-5, tol_mean=1e-6)
@@ -160,9 +163,11 @@ def test_coarse_levels_bitwise_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, param
 
 
 # ---- single level: K fused sweeps vs `iterations` oracle sweeps ---------------
+@pytest.mark.parametrize("kernel", [1, 2])
 @pytest.mark.parametrize("w,h,K", [(37, 29, 1), (64, 64, 2), (100, 70, 3), (130, 97, 4), (50, 40, 8), (33, 200, 10),
-                                   (1, 50, 2), (50, 1, 2), (300, 33, 2), (257, 129, 2)])
-def test_sweep_passes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, K):
+                                   (1, 50, 2), (50, 1, 2), (300, 33, 2), (257, 129, 2), (700, 300, 2), (520, 260, 4),
+                                   (333, 190, 1)])
+def test_sweep_passes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, K, kernel):
     rng = np.random.default_rng(w * 31 + h * 7 + K)
     img = rng.random((3, h, w)).astype(np.float32)
     a = rng.random((h, w)).astype(np.float32)
@@ -171,7 +176,8 @@ def test_sweep_passes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, K):
     p = oracle_mod.Params()
     of, ob = orc.sweep(img.astype(np.float64), a.astype(np.float64), f0.astype(np.float64), b0.astype(np.float64), p,
                        K)
-    gf, gb = fgm.sweep_passes_cuda(dev(img, cuda), dev(a, cuda), dev(f0, cuda), dev(b0, cuda), K, p.eps_r, p.omega)
+    gf, gb = fgm.sweep_passes_cuda(dev(img, cuda), dev(a, cuda), dev(f0, cuda), dev(b0, cuda), K, p.eps_r, p.omega,
+                                   kernel)
     torch.cuda.synchronize()
     assert_close("fg", gf.double().cpu().numpy(), of, tol_max=2e-5, tol_mean=1e-6)
     assert_close("bg", gb.double().cpu().numpy(), ob, tol_max=2e-5, tol_mean=1e-6)
@@ -586,10 +592,10 @@ def test_stalled_handover_returns_runtime_error(fgm, cuda):
 @pytest.mark.gpu
 def test_k4_throughput_launch_vs_oracle(fgm, cuda, orc, oracle_mod):
     """iters_high = 4 fuses the two big-level sweeps of every big level into one
-    K = 4 pass; 16 images of 1024^2 give 16 x 33 bands x 3 channels = 1584
-    (band, channel) items in the top-level launch, more than the GPU holds at
-    once (148 SMs x 8 warps), so it runs the throughput instantiation
-    (sweep_kernel<4, true, 16>) that config 5 uses at its top level."""
+    K = 4 pass; 16 images of 1024^2 give 16 x 17 bands x 3 channels = 816
+    (band, channel) items of the throughput kernel (sweep.cu) in the top-level
+    launch, more than the GPU holds at once (148 SMs x 5 warps), so it runs the
+    16-column-chunk instantiation sweep_kernel<4, 16>."""
     from paper_2006_14970_b200 import synth
 
     n = 16
