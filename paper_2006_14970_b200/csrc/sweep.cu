@@ -87,49 +87,57 @@ __device__ __forceinline__ void st_relaxed_v2(float* p, float2 v) {
     asm volatile("st.relaxed.gpu.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y));
 }
 extern __shared__ float4 sweep_sm4[];
-__device__ __forceinline__ float* smf() { return reinterpret_cast<float*>(sweep_sm4); }
-__device__ __forceinline__ float lds(int i) { return smf()[i]; }
-__device__ __forceinline__ void sts4(int i, float4 v) { reinterpret_cast<float4*>(smf() + i)[0] = v; }
+__device__ __forceinline__ void sts4(int i, float4 v) { reinterpret_cast<float4*>(reinterpret_cast<float*>(sweep_sm4) + i)[0] = v; }
 __device__ __forceinline__ void stg(float* p, float v) { __stcg(p, v); }
 __device__ __forceinline__ bool is_sentinel(float v) { return __float_as_uint(v) == kStreamSentinel; }
 
 // Shared-memory geometry of one (band, channel) warp, in floats.
 //   rings: [plane][ring row][32 columns], column x at x & 31; ring row = band
-//          row - L_p (alpha rows -K..64, image rows -(K-1)..63, F/B rows 0..64)
+//          row - L_p (alpha rows -K..64, image rows -(K-1)..63, F/B rows
+//          0..64), refilled in 16-column (64-byte) segments.  (16-column F/B
+//          rings with 8-column segments -- F and B are read at one column per
+//          row and step -- would fit 6 warps per SM, but leave one 4-step
+//          group of lead: measured 20% slower, the refill wait stalls on DRAM
+//          latency even with L2 prefetches; profiles/r02/k3_v2_notes.txt)
 //   output ring: [F/B][orow(r)][16 columns]; chunk buffer: [column][k][F, B]
 // Read window of ring row r at step t, relative to t - r: alpha [MA, 1],
-// image [MI, 0], F/B [0, 1] (MA, MI: the recomputed slots and the rows below
-// reading their upper neighbour).  A 16-column segment is refilled when the
-// segment whose ring slot it takes leaves the window.
+// image [MI, 0], F/B [1, 1] (MA, MI: the recomputed slots and the rows below
+// reading their upper neighbour).  A segment is refilled when the segment
+// whose ring slot it takes leaves the window.
 template <int K, int CK>
 struct Geom {
-    static constexpr int RW = 32;
+    static constexpr int RW = 32, RWF = 32;
     static constexpr int LA = -K, NA = BR + 1 + K;
     static constexpr int LI = -(K - 1), NI = BR + K - 1;
     static constexpr int NF = BR + 1;  // F/B rows 0 .. 64
     static constexpr int OFF_A = 0;
     static constexpr int OFF_I = OFF_A + NA * RW;
     static constexpr int OFF_F = OFF_I + NI * RW;
-    static constexpr int OFF_B = OFF_F + NF * RW;
+    static constexpr int OFF_B = OFF_F + NF * RWF;
     static constexpr int OW = 16;
     static constexpr int OPL = (BR + BR / 16) * OW;
-    static constexpr int OFF_O = OFF_B + NF * RW;
+    static constexpr int OFF_O = OFF_B + NF * RWF;
     static constexpr int OFF_C = OFF_O + 2 * OPL;
     static constexpr int CH = CK * K * 2;  // one boundary-stream chunk: [column][k][F, B]
     static constexpr int CH4 = CH / 4;     // float4 per chunk (<= 32: one per lane)
     static constexpr int TOTAL = OFF_C + CH;
-    static constexpr int MA = K >= 2 ? -(2 * K - 1) : -1;
-    static constexpr int MI = -2 * (K - 1);
-    static constexpr int MF = 0;
-    // the refill phase of a plane: issue time - free time, making the rows of
-    // a 4-step group's refills 4 consecutive rows of each 16-row block
-    static constexpr int phase(int m) { return ((m % 4) + 4) % 4; }
-    // a group waits for the refills of the group before last (lead >= 2
-    // groups) when every plane's window leaves >= 8 steps, else the last one
-    static constexpr int lead(int m) { return 15 + m - phase(m) - 3; }
-    static constexpr int WAITN = lead(MA) >= 8 && lead(MI) >= 8 ? 1 : 0;
+    // per plane p (0 alpha, 1 image, 2 F, 3 B): segment width, window
+    static constexpr int sw(int p) { return 16; }
+    static constexpr int mlo(int p) { return p == 0 ? (K >= 2 ? -(2 * K - 1) : -1) : p == 1 ? -2 * (K - 1) : 1; }
+    static constexpr int mhi(int p) { return p == 1 ? 0 : 1; }
+    // the refill phase: issue time - free time, making the rows of a 4-step
+    // group's refills 4 consecutive rows of each segment-width block
+    static constexpr int phase(int p) { return ((mlo(p) % 4) + 4) % 4; }
+    // steps from a refill's issue to its first read
+    static constexpr int lead(int p) { return sw(p) - mhi(p) + mlo(p) - phase(p); }
+    static constexpr int minlead() {
+        return lead(0) < lead(1) ? (lead(0) < lead(2) ? lead(0) : lead(2)) : (lead(1) < lead(2) ? lead(1) : lead(2));
+    }
+    // a group waits for the refills issued two groups back when every lead is
+    // >= 8 steps, else for those of the previous group (then >= 4 steps)
+    static constexpr int WAITN = minlead() >= 8 ? 1 : 0;
     static_assert(CH % 4 == 0 && CH4 <= 32, "a chunk is at most one float4 per lane");
-    static_assert(MA - 1 >= -RW / 2 && lead(MA) >= 4, "read window too wide for the ring");
+    static_assert(minlead() >= 4, "read window too wide for the ring");
 };
 
 __device__ __forceinline__ constexpr int orow(int r) { return r + (r >> 4); }
@@ -171,7 +179,7 @@ struct LaneState {
 struct StepCtx {
     int lane, y0, w, h, Umax;
     unsigned lb4;      // byte offset of ring row 2j in a plane (256 * lane: bits >= 8)
-    unsigned ob4;      // byte offset of output-ring row orow(2j) (bits >= 6)
+    unsigned ob4;      // byte offset of output-ring row orow(2j) (bits >= 7)
     unsigned flb4;     // flush: byte offset of output-ring row 17 * (lane >> 4), column lane & 15
     bool has_up, has_down;
     float* my_stream;  // this band's stream (column 0)
@@ -182,11 +190,18 @@ struct StepCtx {
     float eps, omega;
 };
 
+__device__ __forceinline__ float2 ldsb2(unsigned off) {
+    return *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(sweep_sm4) + off);
+}
+__device__ __forceinline__ void stsb2(unsigned off, float2 v) {
+    *reinterpret_cast<float2*>(reinterpret_cast<char*>(sweep_sm4) + off) = v;
+}
+// (F, B) from the previous lane as one 64-bit shuffle: lands in a register pair
+__device__ __forceinline__ float2 shfl_up_pair(float2 v) {
+    return upk2(__shfl_up_sync(kFull, pk2(v), 1));
+}
 __device__ __forceinline__ float ldsb(unsigned off) {
     return *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sweep_sm4) + off);
-}
-__device__ __forceinline__ void stsb(unsigned off, float v) {
-    *reinterpret_cast<float*>(reinterpret_cast<char*>(sweep_sm4) + off) = v;
 }
 
 // Step variants: X = 0 interior columns, 1 left border region (some x <= 0),
@@ -204,30 +219,28 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
     auto C = [&](int e) { return x_.lb4 | (unsigned(c4g + 4 * (s + e)) & 124u); };
     auto A = [&](int d) { return unsigned(4 * (G::OFF_A + (d - G::LA) * G::RW)); };
     auto Ip = [&](int d) { return unsigned(4 * (G::OFF_I + (d - G::LI) * G::RW)); };
-    auto Fp = [&](int d) { return unsigned(4 * (G::OFF_F + d * G::RW)); };
-    auto Bp = [&](int d) { return unsigned(4 * (G::OFF_B + d * G::RW)); };
+    auto CF = C;
+    auto Fp = [&](int d) { return unsigned(4 * (G::OFF_F + d * G::RWF)); };
+    auto Bp = [&](int d) { return unsigned(4 * (G::OFF_B + d * G::RWF)); };
 
     // values from the row above row 2j: shfl.up of row 2j+1, lane 0 from the chunk
     float2 rv[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        rv[k].x = __shfl_up_sync(kFull, st.o[1][k].x, 1);
-        rv[k].y = __shfl_up_sync(kFull, st.o[1][k].y, 1);
-    }
+    for (int k = 0; k < K; ++k) rv[k] = shfl_up_pair(st.o[1][k]);
     if (lane == 0 && x_.has_up) {
-        const int cn = G::OFF_C + (t & (CK - 1)) * K * 2;
+        const unsigned cn = unsigned(4 * G::OFF_C + (t & (CK - 1)) * K * 8);
 #pragma unroll
-        for (int k = 0; k < K; ++k) rv[k] = make_float2(lds(cn + 2 * k), lds(cn + 2 * k + 1));
+        for (int k = 0; k < K; ++k) rv[k] = ldsb2(cn + 8 * k);
     }
 
     // slot-0 loads: row 2j (x0 = t - 2j), row 2j+1 (x1 = x0 - 1)
     const float aR0 = ldsb(C(1) + A(0)), aR1 = ldsb(C(0) + A(1));
     const float I0 = ldsb(C(0) + Ip(0)), I1 = ldsb(C(-1) + Ip(1));
-    const float2 FR0 = make_float2(ldsb(C(1) + Fp(0)), ldsb(C(1) + Bp(0)));
-    const float2 FR1 = make_float2(ldsb(C(0) + Fp(1)), ldsb(C(0) + Bp(1)));
+    const float2 FR0 = make_float2(ldsb(CF(1) + Fp(0)), ldsb(CF(1) + Bp(0)));
+    const float2 FR1 = make_float2(ldsb(CF(0) + Fp(1)), ldsb(CF(0) + Bp(1)));
     const float aU0 = ldsb(C(0) + A(-1));
     const float aD1 = ldsb(C(-1) + A(2));
-    const float2 FD1 = make_float2(ldsb(C(-1) + Fp(2)), ldsb(C(-1) + Bp(2)));
+    const float2 FD1 = make_float2(ldsb(CF(-1) + Fp(2)), ldsb(CF(-1) + Bp(2)));
 
     const int x0 = t - 2 * lane;
     const int w = x_.w;
@@ -315,13 +328,13 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
         }
     }
 
-    // output ring (last sweep only), row orow(2j + i), column x & 15.  Pixels
-    // outside the image land in slots that are rewritten or never flushed.
+    // output ring (last sweep only), row orow(2j + i), column x & 15, (F, B)
+    // interleaved.  Pixels outside the image land in slots that are
+    // rewritten or never flushed.
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-        const unsigned o = (x_.ob4 + 64u * i) | (unsigned(c4g + 4 * (s - i - (K - 1))) & 60u);
-        stsb(o, nv[i][K - 1].x);
-        stsb(o + 4 * G::OPL, nv[i][K - 1].y);
+        const unsigned o = (x_.ob4 + 128u * i) | (unsigned(2 * (c4g + 4 * (s - i - (K - 1)))) & 120u);
+        stsb2(o, nv[i][K - 1]);
     }
 
     // boundary stream for the band below: the last row's K outputs
@@ -346,7 +359,7 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
     // column x = t - K - 14 - r + (lane & 15)
     {
         const int rho = (t - K - 14) & 15;
-        const unsigned lo = x_.flb4 + 64u * unsigned(rho);
+        const unsigned lo = x_.flb4 + 128u * unsigned(rho);
         const int off0 = rho * x_.op1 + t;
 #pragma unroll
         for (int hb = 0; hb < 2; ++hb) {
@@ -358,10 +371,11 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
                 if (XRm) ok = ok && x < w;
                 if (YE) ok = ok && unsigned(x_.y0 + r - (K - 1)) < unsigned(x_.h);
             }
-            if (ok) {
-                const int off = off0 + hb * 32 * x_.op1;
-                stg(x_.gF + off, ldsb(lo + hb * 34u * 64u));
-                stg(x_.gB + off, ldsb(lo + hb * 34u * 64u + 4u * G::OPL));
+            if (ok) {  // (off >= 0 whenever ok: one IMAD.WIDE.U32 per address)
+                const unsigned off = unsigned(off0 + hb * 32 * x_.op1);
+                const float2 v = ldsb2(lo + hb * 34u * 128u);
+                stg(x_.gF + off, v.x);
+                stg(x_.gB + off, v.y);
             }
         }
         if (XRm && ((w - 1) & (G::OW - 1)) != G::OW - 1) {  // the partial last segment of a row
@@ -371,9 +385,9 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
             if (re >= 0 && re < BR && y >= 0 && y < x_.h && lane < w - xb) {
                 // (lanes < 16: gF = FO + lane - K - 14)
                 const int off = re * (x_.op1 + 1) + xb + K + 14;
-                const unsigned o = unsigned(4 * (G::OFF_O + orow(re) * G::OW + lane));
-                stg(x_.gF + off, ldsb(o));
-                stg(x_.gB + off, ldsb(o + 4u * G::OPL));
+                const float2 v = ldsb2(unsigned(4 * G::OFF_O + 8 * (orow(re) * G::OW + lane)));
+                stg(x_.gF + off, v.x);
+                stg(x_.gB + off, v.y);
             }
         }
     }
@@ -401,11 +415,13 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
 }
 
 // ---- ring refills -----------------------------------------------------------
-// Plane p (0 alpha, 1 image, 2 F, 3 B) of band row r: segment n (columns
-// 16n .. 16n+15) is issued at step 16(n-1) + r - M_p + phase(M_p), when the
-// segment n-2 in its ring slot has left the read window.  In the group of
-// steps [t4, t4+4) that is Z = t4 + M_p - phase(M_p) (a multiple of 4): rows
-// r = 16 beta + (Z & 15) + rho (rho = 0..3) get segment n = (Z >> 4) + 1 - beta.
+// Plane p (0 alpha, 1 image, 2 F, 3 B; segment width SW, ring width 2 SW) of
+// band row r: segment n (columns SW n .. SW n + SW - 1) is issued at step
+// SW (n-1) + r - mlo + phase, when the segment n-2 in its ring slot has left
+// the read window.  In the group of steps [t4, t4+4) that is, with
+// Z = t4 + mlo - phase (a multiple of 4): rows r = SW beta + (Z mod SW) + rho
+// (rho = 0..3) get segment n = (Z div SW) + 1 - beta.  A cp.async instruction
+// covers 32 / SW * 4 ... row segments: lanes = (block, rho, 16-byte piece).
 struct RefillSrc {
     const float* base[4];  // plane row 0 (image row y0), column 0
     int pitch[4];
@@ -423,25 +439,21 @@ __device__ __forceinline__ constexpr int plane_off(int p) {
     return p == 0 ? G::OFF_A : p == 1 ? G::OFF_I : p == 2 ? G::OFF_F : G::OFF_B;
 }
 template <int K, int CK>
-__device__ __forceinline__ constexpr int plane_m(int p) {
-    using G = Geom<K, CK>;
-    return p == 0 ? G::MA : p == 1 ? G::MI : G::MF;
-}
-template <int K, int CK>
 __device__ __forceinline__ constexpr int plane_rows(int p) {
     using G = Geom<K, CK>;
     return p == 0 ? G::NA : p == 1 ? G::NI : G::NF;
 }
+__device__ __forceinline__ constexpr int plane_rw(int p) { return 32; }
 
 // One 16-byte piece (4 columns from c) of plane P, band row r, with every check.
 template <int K, bool V4, int CK, int P>
 __device__ __forceinline__ void put_piece(const RefillSrc& S, unsigned sbase, int r, int c, int y0, int w, int h) {
-    using G = Geom<K, CK>;
+    constexpr int RWp = plane_rw(P);
     if (r < plane_lo<K, CK>(P) || r > plane_hi(P) || c < 0 || c >= w) return;
     const int y = y0 + r;
     if (y < 0 || y >= h) return;
     const float* g = S.base[P] + (long long)r * S.pitch[P] + c;
-    const unsigned d = sbase + 4u * unsigned(plane_off<K, CK>(P) + (r - plane_lo<K, CK>(P)) * G::RW + (c & (G::RW - 1)));
+    const unsigned d = sbase + 4u * unsigned(plane_off<K, CK>(P) + (r - plane_lo<K, CK>(P)) * RWp + (c & (RWp - 1)));
     const int nb = min(w - c, 4);
     if (V4) {
         cp_async16(d, g, nb * 4);
@@ -451,23 +463,33 @@ __device__ __forceinline__ void put_piece(const RefillSrc& S, unsigned sbase, in
     }
 }
 
+// Lane roles of a refill instruction of plane P: piece q of the segment,
+// row rho of the 4-row group, block bsub of the instruction's blocks.
+template <int P>
+struct RefillLane {
+    static constexpr int SW = 16, PPS = SW / 4, BPI = 8 / PPS;  // blocks per instruction
+    int q, rho, bsub;
+    __device__ __forceinline__ explicit RefillLane(int lane) : q(lane % PPS), rho((lane / PPS) & 3), bsub(lane / (4 * PPS)) {}
+};
+
 // The refills of plane P in group t4, every piece checked (band edges, image
 // edges, jobs without 16-byte aligned rows).
 template <int K, bool V4, int CK, int P>
 __device__ __forceinline__ void refill_checked_p(const RefillSrc& S, unsigned sbase, int t4, int lane, int y0, int w,
                                                  int h) {
     using G = Geom<K, CK>;
-    const int q = lane & 3, rho = (lane >> 2) & 3, bl = lane >> 4;
-    constexpr int m = plane_m<K, CK>(P);
-    const int Z = t4 + m - G::phase(m);
-    const int zr = Z & 15, zh = Z >> 4;
-    // beta = -1 .. 4 covers band rows -16 .. 79
+    using RL = RefillLane<P>;
+    constexpr int SW = RL::SW;
+    const RL L(lane);
+    const int Z = t4 + G::mlo(P) - G::phase(P);
+    const int zr = Z & (SW - 1), zh = Z >> (SW == 16 ? 4 : 3);
+    // beta = -1 .. 64 / SW covers band rows -SW .. 64 + SW - 1
 #pragma unroll
-    for (int b0 = -1; b0 <= 3; b0 += 2) {
-        const int beta = b0 + bl;
-        const int r = 16 * beta + zr + rho;
-        const int c0 = 16 * (zh + 1 - beta);
-        if (c0 >= 32) put_piece<K, V4, CK, P>(S, sbase, r, c0 + 4 * q, y0, w, h);
+    for (int b0 = -RL::BPI; b0 <= BR / SW; b0 += RL::BPI) {
+        const int beta = b0 + L.bsub;
+        const int r = SW * beta + zr + L.rho;
+        const int c0 = SW * (zh + 1 - beta);
+        if (c0 >= 2 * SW) put_piece<K, V4, CK, P>(S, sbase, r, c0 + 4 * L.q, y0, w, h);
     }
 }
 template <int K, bool V4, int CK>
@@ -479,39 +501,106 @@ __device__ __forceinline__ void refill_checked(const RefillSrc& S, unsigned sbas
     refill_checked_p<K, V4, CK, 3>(S, sbase, t4, lane, y0, w, h);
 }
 
-// Interior groups of interior bands: every piece of the 4 x 4 main row blocks
-// (band rows 0..63) is inside the image and the job's rows are 16-byte
-// aligned; the extra rows (alpha -K..-1 and 64, image -(K-1)..-1, F/B 64) are
-// refilled in the groups whose phase reaches them.
-template <int K, int CK, int P>
-__device__ __forceinline__ void refill_fast_p(const RefillSrc& S, const float* gl, unsigned ss, int t4, int lane,
-                                              unsigned sbase, int y0, int w, int h) {
+__device__ __forceinline__ void cp_async16_if(unsigned sdst, const float* gsrc, bool pred) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p cp.async.cg.shared.global [%0], [%1], 16;\n}" ::"r"(sdst),
+                 "l"(gsrc), "r"(unsigned(pred))
+                 : "memory");
+}
+
+// The main row blocks of plane P in group t4 (band rows 0..63, two
+// instructions 32 rows apart), for jobs with 16-byte aligned rows.  CHECK:
+// pieces outside the image (rows of a band at the top or bottom, columns at
+// the row ends) or before segment 2 (the prologue's) are predicated off;
+// without CHECK every piece is inside.
+template <int K, int CK, int P, bool CHECK>
+__device__ __forceinline__ void refill_main_p(const RefillSrc& S, int lo_off, unsigned ss, int t4, int lane, int y0,
+                                              int w, int h) {
     using G = Geom<K, CK>;
-    const int bl = lane >> 4;
-    constexpr int m = plane_m<K, CK>(P);
-    const int Z = t4 + m - G::phase(m);
-    const int zr = Z & 15, zh = Z >> 4;
-    const float* g = gl + ((long long)zr * S.pitch[P] + 16 * zh);
-    const unsigned d = ss + 4u * unsigned(plane_off<K, CK>(P) - plane_lo<K, CK>(P) * G::RW) +
-                       unsigned(zr * G::RW * 4 + 64 * ((zh + 1 + bl) & 1));
-    cp_async16f(d, g);
-    cp_async16f(d + 4u * 32u * G::RW, g + 32LL * S.pitch[P] - 32);
-    // extra rows above row 0 (beta = -1) and row 64 (beta = 4)
-    if (P <= 1 && zr == 12) {
-        const int rho = (lane >> 2) & 3, q = lane & 3;
-        if (bl == 0) put_piece<K, true, CK, P>(S, sbase, -4 + rho, 16 * (zh + 2) + 4 * q, y0, w, h);
+    using RL = RefillLane<P>;
+    constexpr int SW = RL::SW, RWp = 2 * SW;
+    const RL L(lane);
+    const int Z = t4 + G::mlo(P) - G::phase(P);
+    const int zr = Z & (SW - 1), zh = Z >> 4;
+    // 32-bit element offsets from the band's plane base (rows 0 .. 63, >= 0
+    // whenever the piece is copied): one IMAD.WIDE.U32 per address
+    const unsigned off = unsigned(lo_off + zr * S.pitch[P] + SW * zh);
+    const float* g = S.base[P] + off;
+    const float* g2 = S.base[P] + (off + unsigned(32 * S.pitch[P] - 32));
+    const unsigned d = ss + 4u * unsigned(plane_off<K, CK>(P) - plane_lo<K, CK>(P) * RWp) +
+                       unsigned(zr * RWp * 4 + 4 * SW * ((zh + 1 + L.bsub) & 1));
+    const unsigned d2 = d + 4u * 32u * RWp;
+    if (CHECK) {
+        const int r = SW * L.bsub + L.rho + zr, c = SW * (zh + 1 - L.bsub) + 4 * L.q;
+        cp_async16_if(d, g, c >= 2 * SW && c < w && unsigned(y0 + r) < unsigned(h));
+        cp_async16_if(d2, g2, c - 32 >= 2 * SW && c - 32 < w && unsigned(y0 + r + 32) < unsigned(h));
+    } else {
+        cp_async16f(d, g);
+        cp_async16f(d2, g2);
     }
-    if (P != 1 && zr == 0) {
-        if (lane < 4) put_piece<K, true, CK, P>(S, sbase, BR, 16 * (zh - 3) + 4 * (lane & 3), y0, w, h);
+}
+
+// The extra ring rows (alpha -K..-1 and 64, image -(K-1)..-1, F and B 64):
+// one lane per 16-byte piece (lanes 0..4K+15), each with a static (plane,
+// row, piece); in the group whose refill rows include its row it copies the
+// row's next segment, with every check.
+struct ExtraLane {
+    const float* base;  // the piece's plane row (band row r), column 4 q
+    unsigned sdst;      // its ring row, column 4 q (bytes)
+    int r, m;           // band row; Z offset of its plane (mlo - phase)
+    int q;
+    bool on;
+};
+
+// (K = 4 has 40 extra pieces: slots 32..39 in a second instruction)
+template <int K>
+__device__ __forceinline__ constexpr bool extra2() { return 8 * K + 8 > 32; }
+
+template <int K, int CK>
+__device__ __forceinline__ ExtraLane make_extra(const RefillSrc& S, unsigned sbase, int slot) {
+    using G = Geom<K, CK>;
+    ExtraLane e;
+    int p = 0;
+    e.q = slot & 3;
+    const int item = slot >> 2;  // alpha -K..-1: items 0..K-1; image -(K-1)..-1: K..2K-2; alpha/F/B 64: 2K-1..2K+1
+    if (item < K) {
+        p = 0;
+        e.r = item - K;
+    } else if (item < 2 * K - 1) {
+        p = 1;
+        e.r = item - K - (K - 1);
+    } else {
+        p = item - (2 * K - 1);  // 0 alpha, 1 -> F (2), 2 -> B (3)
+        if (p > 0) ++p;
+        e.r = BR;
     }
+    e.on = item <= 2 * K + 1;
+    if (!e.on) p = 0, e.r = 0;
+    e.m = p == 0 ? G::mlo(0) - G::phase(0) : p == 1 ? G::mlo(1) - G::phase(1) : G::mlo(2) - G::phase(2);
+    e.base = (p == 0 ? S.base[0] : p == 1 ? S.base[1] : p == 2 ? S.base[2] : S.base[3]) +
+             (long long)e.r * (p <= 1 ? S.pitch[0] : S.pitch[2]) + 4 * e.q;
+    const int lo = p == 0 ? G::LA : p == 1 ? G::LI : 0;
+    const int off = p == 0 ? G::OFF_A : p == 1 ? G::OFF_I : p == 2 ? G::OFF_F : G::OFF_B;
+    e.sdst = sbase + 4u * unsigned(off + (e.r - lo) * 32 + 4 * e.q);
+    return e;
+}
+
+template <int K, int CK>
+__device__ __forceinline__ void refill_extra(const ExtraLane& e, int t4, int y0, int w, int h) {
+    const int Z = t4 + e.m;
+    const int rr = e.r - (Z & 15);
+    const int beta = rr >> 4;  // (arithmetic: rows above the block of Z)
+    const int c = 16 * ((Z >> 4) + 1 - beta) + 4 * e.q;
+    const bool ok = e.on && (rr & 15) < 4 && c >= 32 && c < w && unsigned(y0 + e.r) < unsigned(h);
+    cp_async16_if(e.sdst + 4u * unsigned(c & 31) - 16u * e.q, e.base + (c - 4 * e.q), ok);
 }
 
 // Prologue: segments 0 and 1 of every ring row of plane P.
 template <int K, bool V4, int CK, int P>
 __device__ __forceinline__ void refill_prologue_p(const RefillSrc& S, unsigned sbase, int lane, int y0, int w, int h) {
-    constexpr int N = plane_rows<K, CK>(P) * 8;  // 8 pieces per row: columns 0..31
+    constexpr int PPR = plane_rw(P) / 4;  // pieces per ring row
+    constexpr int N = plane_rows<K, CK>(P) * PPR;
     for (int it = lane; it < N; it += 32)
-        put_piece<K, V4, CK, P>(S, sbase, (it >> 3) + plane_lo<K, CK>(P), 4 * (it & 7), y0, w, h);
+        put_piece<K, V4, CK, P>(S, sbase, it / PPR + plane_lo<K, CK>(P), 4 * (it % PPR), y0, w, h);
 }
 template <int K, bool V4, int CK>
 __device__ __forceinline__ void refill_prologue(const RefillSrc& S, unsigned sbase, int lane, int y0, int w, int h) {
@@ -599,8 +688,8 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     cx.h = h;
     cx.Umax = Umax;
     cx.lb4 = 256u * unsigned(lane);
-    cx.ob4 = unsigned(4 * (G::OFF_O + orow(2 * lane) * G::OW));
-    cx.flb4 = unsigned(4 * (G::OFF_O + 17 * (lane >> 4) * G::OW + (lane & 15)));
+    cx.ob4 = unsigned(4 * G::OFF_O + 8 * orow(2 * lane) * G::OW);
+    cx.flb4 = unsigned(4 * G::OFF_O + 8 * (17 * (lane >> 4) * G::OW + (lane & 15)));
     cx.has_up = q > 0;
     cx.has_down = q < J.nb - 1 && !(fault == 1 && q == 0);  // (fault 1: band 0 never publishes)
     cx.my_stream = J.stream + size_t(sid) * slen;
@@ -630,16 +719,20 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
     S.base[3] = J.bg_in + (long long)ch * J.fstride + (long long)y0 * J.fpitch;
     S.pitch[0] = S.pitch[1] = J.ipitch;
     S.pitch[2] = S.pitch[3] = J.fpitch;
-    // this lane's piece of the main refill blocks: rows 16*bl + rho (+ (Z & 15),
-    // + 32 for the second instruction), columns 16 (1 - bl) + 4 q (+ 16 (Z >> 4))
-    const int bl = lane >> 4, rho = (lane >> 2) & 3, qq = lane & 3;
-    const long long lo0 = 16 * (1 - bl) + 4 * qq;
-    const float* glA = S.base[0] + (long long)(16 * bl + rho) * S.pitch[0] + lo0;
-    const float* glI = S.base[1] + (long long)(16 * bl + rho) * S.pitch[1] + lo0;
-    const float* glF = S.base[2] + (long long)(16 * bl + rho) * S.pitch[2] + lo0;
-    const float* glB = S.base[3] + (long long)(16 * bl + rho) * S.pitch[3] + lo0;
-    const unsigned ss = sbase + 4u * unsigned((16 * bl + rho) * G::RW + 4 * qq);
-
+    // this lane's piece of the main refill blocks: rows SW bsub + rho (+ Z mod
+    // SW; + 32 for the second instruction), columns SW (1 - bsub) + 4 q
+    // (+ SW (Z div SW))
+    int gl[4];
+    unsigned ssl[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int SW = 16, PPS = SW / 4;
+        const int q = lane % PPS, rho = (lane / PPS) & 3, bsub = lane / (4 * PPS);
+        gl[p] = (SW * bsub + rho) * S.pitch[p] + SW * (1 - bsub) + 4 * q;
+        ssl[p] = sbase + 4u * unsigned((SW * bsub + rho) * 2 * SW + 4 * q);
+    }
+    const ExtraLane xtra = make_extra<K, CK>(S, sbase, lane);
+    const ExtraLane xtra2 = make_extra<K, CK>(S, sbase, lane + 32);
     refill_prologue<K, V4, CK>(S, sbase, lane, y0, w, h);
     cp_commit();
     cp_commit();  // (an empty group: the first wait_group<1> covers the prologue)
@@ -700,6 +793,12 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
         } else if (!xl && !xr) {
 #pragma unroll 1
             for (int s = 0; s < 4; ++s) band_step<K, CK, 0, true>(st, cx, c4g, t4, s);
+        } else if (split && !xr && !yband) {
+#pragma unroll 1
+            for (int s = 0; s < 4; ++s) band_step<K, CK, 1, false>(st, cx, c4g, t4, s);
+        } else if (split && !xl && !yband) {
+#pragma unroll 1
+            for (int s = 0; s < 4; ++s) band_step<K, CK, 2, false>(st, cx, c4g, t4, s);
         } else if (split && !xr) {
 #pragma unroll 1
             for (int s = 0; s < 4; ++s) band_step<K, CK, 1, true>(st, cx, c4g, t4, s);
@@ -712,12 +811,21 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
         }
         __syncwarp();  // every lane is done with the ring slots the refills overwrite
         if (rf_band && t4 >= rf_lo && t4 < rf_hi) {
-            refill_fast_p<K, CK, 0>(S, glA, ss, t4, lane, sbase, y0, w, h);
-            refill_fast_p<K, CK, 1>(S, glI, ss, t4, lane, sbase, y0, w, h);
-            refill_fast_p<K, CK, 2>(S, glF, ss, t4, lane, sbase, y0, w, h);
-            refill_fast_p<K, CK, 3>(S, glB, ss, t4, lane, sbase, y0, w, h);
+            refill_main_p<K, CK, 0, false>(S, gl[0], ssl[0], t4, lane, y0, w, h);
+            refill_main_p<K, CK, 1, false>(S, gl[1], ssl[1], t4, lane, y0, w, h);
+            refill_main_p<K, CK, 2, false>(S, gl[2], ssl[2], t4, lane, y0, w, h);
+            refill_main_p<K, CK, 3, false>(S, gl[3], ssl[3], t4, lane, y0, w, h);
+            refill_extra<K, CK>(xtra, t4, y0, w, h);
+            if (extra2<K>()) refill_extra<K, CK>(xtra2, t4, y0, w, h);
+        } else if (V4) {
+            refill_main_p<K, CK, 0, true>(S, gl[0], ssl[0], t4, lane, y0, w, h);
+            refill_main_p<K, CK, 1, true>(S, gl[1], ssl[1], t4, lane, y0, w, h);
+            refill_main_p<K, CK, 2, true>(S, gl[2], ssl[2], t4, lane, y0, w, h);
+            refill_main_p<K, CK, 3, true>(S, gl[3], ssl[3], t4, lane, y0, w, h);
+            refill_extra<K, CK>(xtra, t4, y0, w, h);
+            if (extra2<K>()) refill_extra<K, CK>(xtra2, t4, y0, w, h);
         } else {
-            refill_checked<K, V4, CK>(S, sbase, t4, lane, y0, w, h);
+            refill_checked<K, false, CK>(S, sbase, t4, lane, y0, w, h);
         }
         cp_commit();
     }
