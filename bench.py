@@ -237,7 +237,8 @@ def time_configs(fgm, synth, torch, dev, peak):
         out[cfg.name] = {"size": f"{cfg.width}x{cfg.height}", "iters_high": cfg.iters_high,
                          "ms_per_solve": round(med, 4), "mp_per_s": round(mp / (med / 1e3), 1),
                          "k3_ms": round(k3_ms, 4), "k3_gbs": round(achieved, 1),
-                         "k3_roofline_frac": round(achieved / peak, 4), "reps": reps}
+                         "k3_roofline_frac": round(achieved / peak, 4), "reps": reps,
+                         "k3_kernel": "latency kernel (sweep_lat.cu, 32-row bands): a single image is chain-bound"}
         del img, a, fg, bg
         torch.cuda.empty_cache()
     return out
@@ -378,7 +379,8 @@ def run_ours(args, rank, world, local):
                     "steps": e2e_steps, "entry": "fgm_batch_solve_host_f32 (C ABI, pinned host buffers)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "kernel": "sweep_kernel (K3), every launch of a step", "peak_kind": peak_kind,
+                         "kernel": "sweep_kernel (K3), every launch of a step: the throughput kernel (sweep.cu, "
+                                   "64-row bands, two rows per lane; batches)", "peak_kind": peak_kind,
                          "alg_bytes_per_px_pass": ALG_BYTES_PER_PX_PASS,
                          "scope": "achieved = sum of 64 B x level pixels over the step's K3 passes / sum of their "
                                   "CUDA-event durations; traffic = ncu dram__bytes_read+write summed over the same "

@@ -2,6 +2,7 @@
 
     python tools/summarize_ncu.py launches <launches.csv> <out.txt>
     python tools/summarize_ncu.py full <report.ncu-rep> <out.txt> [<traffic.json> <alg_bytes_per_launch>]
+    python tools/summarize_ncu.py traffic <dram.csv> <traffic.json> <alg_bytes_per_step>
 """
 import collections
 import csv
@@ -83,8 +84,33 @@ def full(rep, out, traffic=None, alg=None):
         print(info)
 
 
+def traffic(path, out, alg):
+    """DRAM bytes of every K3 launch of one step (ncu --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum,gpu__time_duration.sum over the step's sweep launches)."""
+    text = open(path).read()
+    rd = csv.DictReader(io.StringIO(text[text.find('"ID"'):]))
+    per = collections.defaultdict(dict)
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+             "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+    for r in rd:
+        per[r["ID"]][r["Metric Name"]] = float(r["Metric Value"].replace(",", "")) * scale.get(r["Metric Unit"], 1.0)
+        per[r["ID"]]["name"] = r["Kernel Name"]
+    launches_ = [v for _, v in sorted(per.items(), key=lambda x: int(x[0]))]
+    tb = sum(v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in launches_)
+    info = {"kernel": launches_[0]["name"].split("(")[0], "launches_per_step": len(launches_),
+            "dram_bytes_per_step": tb, "alg_bytes_per_step": float(alg), "traffic_over_alg": tb / float(alg),
+            "per_launch": [{"dram_bytes": v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"],
+                            "ms_serialised": v.get("gpu__time_duration.sum")} for v in launches_],
+            "source": path, "note": "every K3 launch of one C4 batch solve (tools/prof_batch.py 256), ncu "
+                                    "--metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none"}
+    json.dump(info, open(out, "w"), indent=1)
+    print(json.dumps(info, indent=1))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "traffic":
+        traffic(*sys.argv[2:])
     else:
         full(*sys.argv[2:])
