@@ -392,6 +392,9 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx& x_, i
         }
     }
 
+    // every lane's flush reads are done before the next step's output-ring
+    // stores reuse the slots (lanes of a diverged warp may run ahead)
+    __syncwarp();
     // carry
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -791,7 +794,11 @@ __device__ __forceinline__ void run_band(const SweepJob& J, int q, int ch, int l
 #pragma unroll
             for (int s = 0; s < 4; ++s) band_step<K, CK, 0, false>(st, cx, c4g, t4, s);
         } else if (!xl && !xr) {
+#ifdef FGM_Y_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
             for (int s = 0; s < 4; ++s) band_step<K, CK, 0, true>(st, cx, c4g, t4, s);
         } else if (split && !xr && !yband) {
 #pragma unroll 1
@@ -904,7 +911,7 @@ cudaError_t launch_sweep_k(const SweepArgs& A, cudaStream_t s) {
 
 __global__ void stream_fill_kernel(const SweepJob* __restrict__ jobs, int K) {
     const SweepJob J = jobs[blockIdx.y];
-    const size_t n = size_t(J.nb) * 3 * sweep_stream_len(J.w, K) / 4;
+    const size_t n = (size_t(J.nb) * (3 * sweep_stream_len(J.w, K) + (J.cs ? sweep_cstream_len(J.w, K) : 0))) / 4;
     float4* p = reinterpret_cast<float4*>(J.stream);
     const float s = __uint_as_float(kStreamSentinel);
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)

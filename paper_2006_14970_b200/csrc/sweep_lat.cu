@@ -623,6 +623,9 @@ __device__ __forceinline__ void band_step(LaneState<K>& st, const StepCtx<K>& x_
         }
     }
 
+    // every lane's flush reads are done before the next step's output-ring
+    // stores reuse the slots (lanes of a diverged warp may run ahead)
+    __syncwarp();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         if (G || Y || XL) st.rprev[k] = recv[k];
