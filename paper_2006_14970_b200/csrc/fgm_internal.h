@@ -113,7 +113,6 @@ struct SweepJob {
     int ipitch, fpitch, opitch;           // row strides of the same
     int w, h, nb, band_base;
     int vec4;            // all input rows 16-byte aligned (pitches % 4 == 0, aligned bases): 16-byte cp.async
-    int cs;              // the latency kernel's per-band coefficient streams follow the 3 * nb F/B streams
 };
 
 // A job of one sweep launch is split into (band, channel) work items: band q,
@@ -127,14 +126,8 @@ inline int sweep_bands(int h, int K, int rows = kBandRows) { return (h + K - 1 +
 __host__ __device__ inline size_t sweep_stream_len(int w, int K) {
     return (size_t(w + K - 1) * size_t(K) * 2 + 3) / 4 * 4;
 }
-// The latency kernel's (sweep_ws.cu) coefficient stream of one band: per
-// column, the 8-float records of its last K-1 rows.
-__host__ __device__ inline size_t sweep_cstream_len(int w, int K) {
-    return K > 1 ? (size_t(w + K - 1) * size_t(K - 1) * 8 + 3) / 4 * 4 : 0;
-}
 inline size_t sweep_stream_floats(int w, int h, int K, int rows = kBandRows) {
-    const size_t nb = size_t(sweep_bands(h, K, rows));
-    return nb * 3 * sweep_stream_len(w, K) + (rows == kLatBandRows ? nb * sweep_cstream_len(w, K) : 0);
+    return size_t(sweep_bands(h, K, rows)) * 3 * sweep_stream_len(w, K);
 }
 // Launch helpers (kernels.cu).  `jobs_dev` are device copies of the arrays.
 // Tiles of 128 x 8 destination pixels; total_tiles = sum over jobs.
@@ -165,10 +158,6 @@ cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev,
 // sweep_lat.cu).
 cudaError_t launch_sweep_lat(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
                              float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
-// Experimental: the warp-specialised latency kernel (sweep_ws.cu), which needs
-// the coefficient streams (SweepJob::cs).
-cudaError_t launch_sweep_ws(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
-                            float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
 extern std::atomic<int> g_sweep_fault;            // debug fault injection (fgm_debug_fault)
 extern std::atomic<long long> g_spin_timeout_ns;  // bound on one boundary-stream wait
 // Fill every job's boundary streams with kStreamSentinel (before its sweep).

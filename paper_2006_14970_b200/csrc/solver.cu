@@ -482,12 +482,11 @@ int read_faults() {
 }
 
 // ticket[0]: the launch's band ticket, ticket[1]: its abort flag (both zeroed)
-// kern: 0 the throughput kernel, 1 the latency kernel (kLatBandRows-row
-// bands), 3 the experimental warp-specialised latency kernel (same bands)
+// lat: the jobs are cut into kLatBandRows-row bands for the latency kernel
 cudaError_t launch_sweep_passes(int K, const SweepJob* jd, const int2* od, int bands, unsigned* ticket, float eps,
-                                float omega, int kern, cudaStream_t s) {
-    auto f = kern == 0 ? launch_sweep : kern == 3 ? launch_sweep_ws : launch_sweep_lat;
-    return f(K, jd, od, 3 * bands, ticket, eps, omega, reinterpret_cast<int*>(ticket + 1), device_fault_counter(), s);
+                                float omega, bool lat, cudaStream_t s) {
+    return (lat ? launch_sweep_lat : launch_sweep)(K, jd, od, 3 * bands, ticket, eps, omega,
+                                                   reinterpret_cast<int*>(ticket + 1), device_fault_counter(), s);
 }
 
 enum LaunchKind { kCoarse, kResample, kUpsample, kSweep, kCopy, kPyramid };
@@ -785,7 +784,6 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                     J1.nb = sweep_bands(L.h, K, rows);
                     J1.band_base = total;
                     J1.vec4 = vec4_ok(J1);
-                    J1.cs = lat ? 1 : 0;
                     total += J1.nb;
                     max_stream = std::max(max_stream, sweep_stream_floats(L.w, L.h, K, rows));
                     sbytes += 64.0 * double(px);
@@ -895,7 +893,7 @@ void solve_batch(std::vector<ImageIO>& ios, const fgm_params* p, cudaStream_t s)
                 ProfScope ps(s, 0, r.bytes);
                 const SweepJob* jd = reinterpret_cast<const SweepJob*>(djobs + r.job_off);
                 const int2* od = reinterpret_cast<const int2*>(djobs + r.order_off);
-                ck(launch_sweep_passes(r.K, jd, od, r.total_bands, dctr + r.ticket, eps, omega, r.lat, s),
+                ck(launch_sweep_passes(r.K, jd, od, r.total_bands, dctr + r.ticket, eps, omega, r.lat != 0, s),
                    "sweep_kernel");
                 break;
             }
@@ -1309,9 +1307,8 @@ int fgm_sweep_passes_kernel_f32(const float* image, const float* alpha, const fl
     return guarded([&] {
         check_dims(w, h);
         if (iterations < 1) throw InvalidArgument("MlParams: iteration counts must be >= 1");
-        if (kernel < 0 || kernel > 3) throw InvalidArgument("sweep kernel must be 0 (automatic), 1, 2 or 3");
+        if (kernel < 0 || kernel > 2) throw InvalidArgument("sweep kernel must be 0 (automatic), 1 or 2");
         const bool lat = kernel != 2;  // one image: latency-bound
-        const int kern = kernel == 2 ? 0 : kernel == 3 ? 3 : 1;
         const int rows = lat ? kLatBandRows : kBandRows;
         fgm_params p{regularization, gradient_weight, 1, 1, 1};
         validate(&p);
@@ -1350,7 +1347,6 @@ int fgm_sweep_passes_kernel_f32(const float* image, const float* alpha, const fl
             J1.nb = sweep_bands(h, ps[pi], rows);
             J1.band_base = 0;
             J1.vec4 = vec4_ok(J1);
-            J1.cs = lat ? 1 : 0;
             ck(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned), s), "memset");
             SweepJob* d = A.take<SweepJob>(1);
             ck(cudaMemcpyAsync(d, &J1, sizeof(J1), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(jobs)");
@@ -1361,7 +1357,7 @@ int fgm_sweep_passes_kernel_f32(const float* image, const float* alpha, const fl
             ck(launch_stream_fill(d, 1, ps[pi], sf, s), "stream_fill_kernel");
             {
                 ProfScope pr(s, 0, 64.0 * double(px));
-                ck(launch_sweep_passes(ps[pi], d, dord, J1.nb, ctr, float(regularization), float(gradient_weight), kern,
+                ck(launch_sweep_passes(ps[pi], d, dord, J1.nb, ctr, float(regularization), float(gradient_weight), lat,
                                        s),
                    "sweep_kernel");
             }

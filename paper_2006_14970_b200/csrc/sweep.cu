@@ -911,7 +911,7 @@ cudaError_t launch_sweep_k(const SweepArgs& A, cudaStream_t s) {
 
 __global__ void stream_fill_kernel(const SweepJob* __restrict__ jobs, int K) {
     const SweepJob J = jobs[blockIdx.y];
-    const size_t n = (size_t(J.nb) * (3 * sweep_stream_len(J.w, K) + (J.cs ? sweep_cstream_len(J.w, K) : 0))) / 4;
+    const size_t n = size_t(J.nb) * 3 * sweep_stream_len(J.w, K) / 4;
     float4* p = reinterpret_cast<float4*>(J.stream);
     const float s = __uint_as_float(kStreamSentinel);
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
