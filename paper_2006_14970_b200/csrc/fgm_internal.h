@@ -158,6 +158,11 @@ cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev,
 // sweep_lat.cu).
 cudaError_t launch_sweep_lat(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
                              float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
+// The warp-specialised latency kernel (sweep_ws.cu): one CTA per 32-row band,
+// a producer warp computing the alpha-only coefficients once per pixel and one
+// chain warp per channel running the recurrence.  Same jobs, order and streams.
+cudaError_t launch_sweep_ws(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
+                            float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
 extern std::atomic<int> g_sweep_fault;            // debug fault injection (fgm_debug_fault)
 extern std::atomic<long long> g_spin_timeout_ns;  // bound on one boundary-stream wait
 // Fill every job's boundary streams with kStreamSentinel (before its sweep).

@@ -75,12 +75,12 @@ def test_ml_vs_oracle_params(fgm, cuda, orc, oracle_mod, kw):
     assert_close("bg", b, ob)
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 @pytest.mark.parametrize("w,h", [(7, 100), (37, 65), (39, 200), (40, 33), (41, 31), (64, 97), (300, 32), (300, 33),
                                  (90, 130), (200, 129), (123, 64), (96, 66)])
 def test_sweep_border_modes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, kernel):
     # narrow levels and bands at the row borders: the border / row-border /
-    # band-start variants of both K3 kernels (sweep_lat.cu: 1, sweep.cu: 2)
+    # band-start variants of the K3 kernels (sweep_lat.cu: 1, sweep.cu: 2, sweep_ws.cu: 3)
     # against the fp64 oracle, level by level through the single-level entry
     # (BASELINE params, K = 1..4)
     rng = np.random.default_rng(w * 1000 + h)
@@ -163,7 +163,7 @@ def test_coarse_levels_bitwise_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, param
 
 
 # ---- single level: K fused sweeps vs `iterations` oracle sweeps ---------------
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 @pytest.mark.parametrize("w,h,K", [(37, 29, 1), (64, 64, 2), (100, 70, 3), (130, 97, 4), (50, 40, 8), (33, 200, 10),
                                    (1, 50, 2), (50, 1, 2), (300, 33, 2), (257, 129, 2), (700, 300, 2), (520, 260, 4),
                                    (333, 190, 1)])
