@@ -161,6 +161,8 @@ cudaError_t launch_sweep_lat(int K, const SweepJob* jobs_dev, const int2* order_
 // The warp-specialised latency kernel (sweep_ws.cu): one CTA per 32-row band,
 // a producer warp computing the alpha-only coefficients once per pixel and one
 // chain warp per channel running the recurrence.  Same jobs, order and streams.
+// ws_band_capacity(): band CTAs resident at once on the current device.
+cudaError_t ws_band_capacity(int K, int& cap);
 cudaError_t launch_sweep_ws(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
                             float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
 extern std::atomic<int> g_sweep_fault;            // debug fault injection (fgm_debug_fault)

@@ -489,7 +489,15 @@ std::atomic<int> g_lat_kernel{3};
 
 cudaError_t launch_sweep_passes(int K, const SweepJob* jd, const int2* od, int bands, unsigned* ticket, float eps,
                                 float omega, bool lat, cudaStream_t s, int lat_kernel = 0) {
-    if (!lat_kernel) lat_kernel = g_lat_kernel.load();
+    if (lat && !lat_kernel) {
+        // automatic: the band CTAs of the warp-specialised kernel hold one band
+        // per SM; a launch with more than two rounds of bands (a 16384^2 level)
+        // is bound by resident bands, where the one-warp kernel's 9 warps per
+        // SM win (measured, profiles/r02/k3_ws_notes.txt)
+        lat_kernel = g_lat_kernel.load();
+        int cap = 0;
+        if (lat_kernel == 3 && ws_band_capacity(K, cap) == cudaSuccess && bands > 2 * cap) lat_kernel = 1;
+    }
     auto fn = !lat ? launch_sweep : lat_kernel == 3 ? launch_sweep_ws : launch_sweep_lat;
     return fn(K, jd, od, 3 * bands, ticket, eps, omega, reinterpret_cast<int*>(ticket + 1), device_fault_counter(), s);
 }

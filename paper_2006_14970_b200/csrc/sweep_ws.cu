@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 
 #include "fgm_device.cuh"
 #include "fgm_internal.h"
@@ -79,12 +80,18 @@ __device__ __forceinline__ void st_relaxed_v4(float* p, float4 v) {
 __device__ __forceinline__ void st_relaxed_v2(float* p, float2 v) {
     asm volatile("st.relaxed.gpu.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y));
 }
-__device__ __forceinline__ void st_release_cta(unsigned saddr, int v) {
-    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+// The progress protocol runs without fences (a fence drains the warp's
+// outstanding cp.async and global stores: 200-700 cycles per group, measured
+// with st.release / ld.acquire): shared-memory accesses of one SM are served
+// in issue order, so a volatile store issued after the warp's record accesses
+// (__syncwarp) cannot overtake them, and record reads issued after a volatile
+// load that saw the counter see the records stored before it.
+__device__ __forceinline__ void st_volatile_cta(unsigned saddr, int v) {
+    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
-__device__ __forceinline__ int ld_acquire_cta(unsigned saddr) {
+__device__ __forceinline__ int ld_volatile_cta(unsigned saddr) {
     int v;
-    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
     return v;
 }
 
@@ -139,12 +146,16 @@ struct Geom {
     static constexpr int AW = 64;        // alpha ring columns
     static constexpr int ARS = AW + 4;   // ARS - 1 odd
     static constexpr int NA = 33 + K;    // alpha ring rows: band rows -K..32
-    static constexpr int MA = 8;         // alpha load groups in flight
-    static constexpr int LA = S * MA;    // alpha load lead: S*MA - S + 3 + W1, W1 = 1
+    static constexpr int MA = 4;         // alpha load iterations in flight (an iteration: 2S columns)
+    static constexpr int LA = 2 * S * MA;  // alpha load lead: 2S*MA - S + 3 + W1, W1 = 1
     static constexpr int OFF_AL = REC_B + NR * RS * 4;
-    static constexpr int OFF_PR = OFF_AL + NA * ARS;  // progress words: producer, chain 0..2
-    static constexpr int TOTAL = OFF_PR + 4;
-    static_assert(L + (2 * K - 3) + S <= RW, "image ring too small for its lead");
+    static constexpr int OFF_PR = OFF_AL + 2 * NA * ARS;  // progress words (one alpha ring per producer)
+    static constexpr int PR_PROD = 0;                     // producers 0, 1: iterations finished
+    static constexpr int PR_CHAIN = 2;                    // chain warps 0..2: groups finished
+    static constexpr int PR_LOAD = 5;                     // helpers 0..2: chain groups whose ring data has landed
+    static constexpr int NPR = 8;
+    static constexpr int TOTAL = OFF_PR + NPR;
+    static_assert(L + 3 + (2 * K - 3) + 2 * S <= RW + 3, "image ring too small for its lead");
     static_assert(K + 1 <= MIR && MIR % 4 == 0 && RS % 4 == 0, "mirror too narrow");
     static_assert(CH % 4 == 0 && CH4 <= 32, "a chunk is at most one float4 per lane");
     static_assert(LA + S + 3 + 2 <= AW, "alpha ring too small for its lead");
@@ -260,7 +271,7 @@ __device__ __forceinline__ FlatSrc<K> make_flat(const SweepJob& J, int ch, int y
         } else {
             p = -1;
         }
-        const int y = min(max(y0 + r, 0), J.h - 1);  // (in range for interior bands)
+        const int y = min(max(y0 + r, 0), J.h - 1);  // (clamped for the first and last band: such ring rows are never read)
         const float* base = p == 0 ? J.img + ch * J.istride + (long long)y * J.ipitch
                           : p == 1 ? J.fg_in + ch * J.fstride + (long long)y * J.fpitch
                                    : J.bg_in + ch * J.fstride + (long long)y * J.fpitch;
@@ -350,17 +361,16 @@ __device__ __forceinline__ bool acquire_chunk(float4 v, const float* up_stream, 
     return true;
 }
 
-// Wait until the progress word at `saddr` reaches `need` (monotonic counter,
-// released by its writer); returns the value seen, or -1 when aborted.
+// Wait until the progress word at `saddr` reaches `need` (a monotonic
+// counter); returns the value seen, or -1 when aborted.  Called by a converged
+// warp: every lane reads the same word in the same instruction (a broadcast),
+// so the value and the branches on it are warp-uniform.
 __device__ __forceinline__ int wait_progress(unsigned saddr, int need, int lane, const SweepFail& F) {
-    // every lane reads the word (one address: a broadcast) and lane 0's value
-    // decides for the warp; the caller's __syncwarp orders the other lanes'
-    // later shared-memory reads after lane 0's acquire
     unsigned long long t0 = 0;
-    int v = __shfl_sync(kFull, ld_acquire_cta(saddr), 0);
+    int v = ld_volatile_cta(saddr);
     for (unsigned n = 0; v < need; ++n) {
         if (!keep_waiting(n, t0, lane, F)) return -1;
-        v = __shfl_sync(kFull, ld_acquire_cta(saddr), 0);
+        v = ld_volatile_cta(saddr);
     }
     return v;
 }
@@ -444,12 +454,14 @@ __device__ __forceinline__ GroupAddr<K> group_addr(const ChainCtx<K>& x_, int t4
 }
 
 // One wavefront step of a chain warp: no barrier inside.  G: a pixel of this
-// step may be on the image border (clamped neighbours).  Y (G false): interior
-// columns of a band touching row 0 or h-1.  XL (G false): the first steps of
-// a band (x <= 0 only).
-template <int K, bool G, int CK, bool Y = false, bool XL = false>
+// step may be on the image border (clamped neighbours).  YU / YD (G false):
+// interior columns of a band touching row 0 / row h-1 (the first band heads
+// every chain: it pays for the U clamp only).  XL (G false): the first steps
+// of a band (x <= 0 only).
+template <int K, bool G, int CK, bool YU = false, bool YD = false, bool XL = false>
 __device__ __forceinline__ void chain_step(LaneState<K>& st, const ChainCtx<K>& x_, int tr,
                                            const GroupAddr<K>* ga = nullptr, int gs = 0) {
+    constexpr bool Y = YU || YD;
     using Gm = Geom<K, CK>;
     const int lane = x_.lane, y0 = x_.y0, w = x_.w, h = x_.h;
     const int c = (tr - lane - Gm::SH) & (Gm::RW - 1);
@@ -489,8 +501,10 @@ __device__ __forceinline__ void chain_step(LaneState<K>& st, const ChainCtx<K>& 
             if (G) {
                 if (!(x < w - 1)) R = self;
             }
-            if (G || Y) {
+            if (G || YU) {
                 if (!(y > 0)) U = self;
+            }
+            if (G || YD) {
                 if (!(y < h - 1)) D = self;
             }
         }
@@ -596,40 +610,79 @@ __device__ __forceinline__ void flush_step(const ChainCtx<K>& x_, int tr, const 
 #ifndef FGM_REPOLL
 #define FGM_REPOLL 1
 #endif
-// Returns false when the launch was aborted.
-template <int K, bool V4, int CK>
-__device__ __forceinline__ bool run_chain(const SweepJob& J, int q, int ch, int lane, unsigned sbase, const SweepFail& F,
-                                          int fault) {
-    using Gm = Geom<K, CK>;
-    const int w = J.w, h = J.h;
-    const int y0 = q * kRows;
-    const int Umax = w + K - 1;
-    const size_t slen = sweep_stream_len(w, K);
-    const int sid = q * 3 + ch;
-    const float* up_stream = q > 0 ? J.stream + size_t(sid - 3) * slen : nullptr;
+#ifdef FGM_WS_TRACE  // development probe: cycles per phase of a warp
+#define TR_DECL long long tr_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tr_t = clock64(), tr_start = tr_t
+#define TR(i)                           \
+    {                                   \
+        const long long c_ = clock64(); \
+        tr_[i] += c_ - tr_t;            \
+        tr_t = c_;                      \
+    }
+#else
+#define TR_DECL
+#define TR(i)
+#endif
 
+// What the three warps of a channel and the producers share about a band.
+template <int K, int CK>
+struct BandGeo {
+    using Gm = Geom<K, CK>;
+    int w, h, y0, Umax, tend, ngroups;
+    bool yband, ytop;
+    int fast_lo, fast_hi;
+    __device__ __forceinline__ BandGeo(const SweepJob& J, int q) {
+        w = J.w;
+        h = J.h;
+        y0 = q * kRows;
+        Umax = w + K - 1;
+        tend = 31 + Umax;  // lane 31's last column is Umax - 1
+        ngroups = (tend + Gm::S + Gm::S - 1) / Gm::S;  // groups t4 = -S, 0, S, ...
+        yband = y0 - (K - 1) <= 0 || y0 + 31 >= h - 1;
+        ytop = y0 + 31 < h - 1;  // (with yband: the band touches row 0 only)
+        fast_lo = 32 + K;  // a step tr has no column border iff fast_lo <= tr < fast_hi
+        fast_hi = w - 2;
+    }
+};
+
+template <int K>
+__device__ __forceinline__ ChainCtx<K> make_ctx(const SweepJob& J, int q, int ch, int lane, int fault) {
+    using Gm = Geom<K>;
+    const int y0 = q * kRows;
+    const size_t slen = sweep_stream_len(J.w, K);
     ChainCtx<K> cx;
     cx.cb = ch * Gm::CHSZ;
     cx.lb = cx.cb + lane * Gm::RS;
     cx.rb = 4 * lane * Gm::RS;
     cx.lane = lane;
     cx.y0 = y0;
-    cx.w = w;
-    cx.h = h;
+    cx.w = J.w;
+    cx.h = J.h;
     cx.has_up = q > 0;
     cx.has_down = q < J.nb - 1 && !(fault == 1 && q == 0);  // (fault 1: band 0 never publishes)
-    cx.Umax = Umax;
-    cx.my_stream = J.stream + size_t(sid) * slen;
+    cx.Umax = J.w + K - 1;
+    cx.my_stream = J.stream + size_t(q * 3 + ch) * slen;
+    // band-relative output base (row y0 - (K-1) may be negative for the first
+    // band: only the pointer arithmetic goes there, stores are bounds-checked)
     cx.FO = J.fg_out + (long long)ch * J.ostride + (long long)(y0 - (K - 1)) * J.opitch;
     cx.BO = J.bg_out + (long long)ch * J.ostride + (long long)(y0 - (K - 1)) * J.opitch;
     cx.opitch = J.opitch;
+    return cx;
+}
 
-    const unsigned cbase = sbase + 4u * unsigned(cx.cb);
-    const RowSrc own = make_rowsrc<K>(J, ch, y0, lane, true, true, cbase);
-    const bool has_x = lane >= 33 - K || lane == 0;
-    const RowSrc ext = make_rowsrc<K>(J, ch, y0, lane == 0 ? 32 : lane - 32, lane >= 33 - K, lane == 0, cbase);
-    const FlatSrc<K> flat = make_flat<K>(J, ch, y0, lane, cbase);
-    const unsigned pr_prod = sbase + 4u * unsigned(Gm::OFF_PR), pr_mine = pr_prod + 4u * unsigned(1 + ch);
+// Chain warp of channel ch: the recurrence only.  Group n starts once the
+// channel's helper has the group's ring data in shared memory and the
+// producers have finished groups n and n + 1.  Returns false when the launch
+// was aborted.
+template <int K, int CK>
+__device__ __forceinline__ bool run_chain(const SweepJob& J, int q, int ch, int lane, unsigned sbase, const SweepFail& F,
+                                          int fault) {
+    using Gm = Geom<K, CK>;
+    const BandGeo<K, CK> bg(J, q);
+    const int Umax = bg.Umax;
+    const ChainCtx<K> cx = make_ctx<K>(J, q, ch, lane, fault);
+    const float* up_stream = q > 0 ? J.stream + size_t((q - 1) * 3 + ch) * sweep_stream_len(J.w, K) : nullptr;
+    const unsigned pr = sbase + 4u * unsigned(Gm::OFF_PR);
+    const unsigned pr_mine = pr + 4u * unsigned(Gm::PR_CHAIN + ch), pr_load = pr + 4u * unsigned(Gm::PR_LOAD + ch);
 
     LaneState<K> st;
 #pragma unroll
@@ -637,35 +690,38 @@ __device__ __forceinline__ bool run_chain(const SweepJob& J, int q, int ch, int 
 
     constexpr int S = Gm::S;
     constexpr int t0 = -S;
-    prologue_row<K, V4>(own, t0, w);
-    if (has_x) prologue_row<K, V4>(ext, t0, w);
-    cp_commit();
-#pragma unroll
-    for (int i = 1; i < Gm::M; ++i) cp_commit();
     float4 pend = make_float4(0.f, 0.f, 0.f, 0.f);
     const bool lane_ch = lane < Gm::CH4;
     bool pend_ok = false;
     if (cx.has_up && lane_ch) pend = ld_relaxed_v4(up_stream + 4 * lane);
 
-    const bool yband = y0 - (K - 1) <= 0 || y0 + 31 >= h - 1;
-    const int fast_lo = 32 + K, fast_hi = w - 2;
-    const int tend = 31 + Umax;
-    const int ngroups = (tend - t0 + S - 1) / S;
-    const int issue_lo = 32 - Gm::L, issue_hi = w - 2 * S - Gm::L - K;
-    int produced = 0;  // cached producer progress (groups finished)
+    int prod0 = 0, prod1 = 0;  // cached producer progress (iterations finished by producer 0 / 1)
+    int loaded = 0;            // cached helper progress (groups whose ring data is in shared memory)
     int n = 0;
-    for (int t4 = t0; t4 < tend; t4 += S, ++n) {
-        cp_wait<Gm::M - 1>();
-        // the records of this group and of the next group's first step
-        const int need = min(n + 2, ngroups);
-        if (produced < need) {
-            produced = wait_progress(pr_prod, need, lane, F);
-            if (produced < 0) {
-                cp_wait<0>();
-                return false;
+    TR_DECL;
+    for (int t4 = t0; t4 < bg.tend; t4 += S, ++n) {
+        TR(0);
+        if (loaded < n + 1) {
+            loaded = wait_progress(pr_load, n + 1, lane, F);
+            if (loaded < 0) return false;
+        }
+        TR(1);
+        // the records of this group and of the next group's first step: the
+        // groups <= g1, of which producer 0 computes the even ones
+        {
+            const int g1 = min(n + 1, bg.ngroups - 1);
+            const int need0 = g1 / 2 + 1, need1 = (g1 + 1) / 2;
+            if (prod0 < need0) {
+                prod0 = wait_progress(pr + 4u * unsigned(Gm::PR_PROD), need0, lane, F);
+                if (prod0 < 0) return false;
+            }
+            if (prod1 < need1) {
+                prod1 = wait_progress(pr + 4u * unsigned(Gm::PR_PROD + 1), need1, lane, F);
+                if (prod1 < 0) return false;
             }
         }
         __syncwarp();
+        TR(2);
         if (t4 < 0) {
             const int c = (-1 - lane - Gm::SH) & (Gm::RW - 1);
 #pragma unroll
@@ -674,10 +730,7 @@ __device__ __forceinline__ bool run_chain(const SweepJob& J, int q, int ch, int 
             if (cx.has_up && t4 < Umax) {
                 const int nxt = (t4 & ~(CK - 1)) + CK;
                 if ((t4 % CK) == 0) {
-                    if (!acquire_chunk<K, CK>(pend, up_stream, t4, Umax, lane, cx.cb + Gm::C_C, F)) {
-                        cp_wait<0>();
-                        return false;
-                    }
+                    if (!acquire_chunk<K, CK>(pend, up_stream, t4, Umax, lane, cx.cb + Gm::C_C, F)) return false;
                     pend_ok = false;
                     if (nxt < Umax && lane_ch) pend = ld_relaxed_v4(up_stream + size_t(nxt) * K * 2 + 4 * lane);
                 } else if (FGM_REPOLL && !pend_ok && nxt < Umax) {
@@ -686,59 +739,131 @@ __device__ __forceinline__ bool run_chain(const SweepJob& J, int q, int ch, int 
                 }
                 __syncwarp();
             }
-            if (t4 >= fast_lo && t4 + S <= fast_hi && !yband) {
+            TR(3);
+            const bool xin = t4 >= bg.fast_lo && t4 + S <= bg.fast_hi;
+            if (xin && !bg.yband) {
                 const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
 #pragma unroll
                 for (int s = 0; s < S; ++s) chain_step<K, false, CK>(st, cx, t4 + s, &ga, s);
-                __syncwarp();
-#pragma unroll
-                for (int s = 0; s < S; ++s) flush_step<K, false, CK>(cx, t4 + s, &ga, s);
-            } else if (t4 >= fast_lo && t4 + S <= fast_hi) {
+            } else if (xin && bg.ytop) {  // the first band of a taller image: U clamps only
                 const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
 #pragma unroll
-                for (int s = 0; s < S; ++s) chain_step<K, false, CK, true>(st, cx, t4 + s, &ga, s);
-                __syncwarp();
-#pragma unroll
-                for (int s = 0; s < S; ++s) flush_step<K, false, CK, true>(cx, t4 + s, &ga, s);
-            } else if (t4 < fast_lo && t4 + S <= fast_hi) {  // band start: left border only
+                for (int s = 0; s < S; ++s) chain_step<K, false, CK, true, false>(st, cx, t4 + s, &ga, s);
+            } else if (xin) {
                 const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
-                if (yband) {
 #pragma unroll
-                    for (int s = 0; s < S; ++s) chain_step<K, false, CK, true, true>(st, cx, t4 + s, &ga, s);
-                    __syncwarp();
+                for (int s = 0; s < S; ++s) chain_step<K, false, CK, true, true>(st, cx, t4 + s, &ga, s);
+            } else if (t4 < bg.fast_lo && t4 + S <= bg.fast_hi) {  // band start: left border only
+                const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
+                if (bg.yband) {
 #pragma unroll
-                    for (int s = 0; s < S; ++s) flush_step<K, false, CK, true, true>(cx, t4 + s, &ga, s);
+                    for (int s = 0; s < S; ++s) chain_step<K, false, CK, true, true, true>(st, cx, t4 + s, &ga, s);
                 } else {
 #pragma unroll
-                    for (int s = 0; s < S; ++s) chain_step<K, false, CK, false, true>(st, cx, t4 + s, &ga, s);
-                    __syncwarp();
-#pragma unroll
-                    for (int s = 0; s < S; ++s) flush_step<K, false, CK, false, true>(cx, t4 + s, &ga, s);
+                    for (int s = 0; s < S; ++s) chain_step<K, false, CK, false, false, true>(st, cx, t4 + s, &ga, s);
                 }
             } else {
 #pragma unroll 1
                 for (int s = 0; s < S; ++s) chain_step<K, true, CK>(st, cx, t4 + s);
-                __syncwarp();
-#pragma unroll 1
-                for (int s = 0; s < S; ++s) flush_step<K, true, CK>(cx, t4 + s);
             }
         }
-        __syncwarp();  // every lane is done with the ring slots the next loads overwrite
-        if (V4 && !yband && t4 >= issue_lo && t4 < issue_hi) {
+        TR(4);
+        __syncwarp();  // every lane's output-ring stores and ring / record reads of the group are issued
+        if (lane == 0) st_volatile_cta(pr_mine, n + 1);
+        TR(5);
+    }
+#ifdef FGM_WS_TRACE
+    if (lane == 0 && ch == 0 && (q == 0 || q == 1 || q == J.nb / 2 || q == J.nb - 1))
+        printf("chain %d/%d K=%d w=%d groups %d: total %lld cyc | loop %lld loadwait %lld prodwait %lld chunk %lld steps %lld "
+               "publish %lld\n",
+               q, J.nb, K, J.w, n, clock64() - tr_start, tr_[0], tr_[1], tr_[2], tr_[3], tr_[4], tr_[5]);
+#endif
+    return true;
+}
+
+// Helper warp of channel ch: streams the channel's I_c / F_c / B_c rows into
+// the rings ahead of the chain warp and flushes its output rows behind it.
+// Iteration i runs once the chain warp has finished group i - 1: it flushes
+// that group's completed output segments, issues the ring blocks "of the end
+// of group i" (they overwrite columns last read in group i - 1), and, after
+// waiting for the blocks issued M - 1 iterations earlier, publishes the ring
+// data of chain group i + 1.
+template <int K, bool V4, int CK>
+__device__ __forceinline__ bool run_helper(const SweepJob& J, int q, int ch, int lane, unsigned sbase, const SweepFail& F,
+                                           int fault) {
+    using Gm = Geom<K, CK>;
+    const BandGeo<K, CK> bg(J, q);
+    const int w = bg.w;
+    const ChainCtx<K> cx = make_ctx<K>(J, q, ch, lane, fault);
+    const unsigned cbase = sbase + 4u * unsigned(cx.cb);
+    const RowSrc own = make_rowsrc<K>(J, ch, bg.y0, lane, true, true, cbase);
+    const bool has_x = lane >= 33 - K || lane == 0;
+    const RowSrc ext = make_rowsrc<K>(J, ch, bg.y0, lane == 0 ? 32 : lane - 32, lane >= 33 - K, lane == 0, cbase);
+    const FlatSrc<K> flat = make_flat<K>(J, ch, bg.y0, lane, cbase);
+    const unsigned pr = sbase + 4u * unsigned(Gm::OFF_PR);
+    const unsigned pr_chain = pr + 4u * unsigned(Gm::PR_CHAIN + ch), pr_mine = pr + 4u * unsigned(Gm::PR_LOAD + ch);
+
+    constexpr int S = Gm::S;
+    constexpr int t0 = -S;
+    prologue_row<K, V4>(own, t0, w);
+    if (has_x) prologue_row<K, V4>(ext, t0, w);
+    cp_commit();
+#pragma unroll
+    for (int i = 1; i < Gm::M; ++i) cp_commit();
+
+    // groups whose issued blocks are inside [0, w) for every row -K .. 32
+    const int issue_lo = 32 - Gm::L, issue_hi = w - 2 * S - Gm::L - K;
+    int chain_done = 0;
+    // flush the output segments completed in group t4 (all of whose steps are done)
+    auto flush_group = [&](int t4) {
+        if (t4 < 0) return;
+        const bool xin = t4 >= bg.fast_lo && t4 + S <= bg.fast_hi;
+        if (xin && !bg.yband) {
+            const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
+#pragma unroll
+            for (int s = 0; s < S; ++s) flush_step<K, false, CK>(cx, t4 + s, &ga, s);
+        } else if (xin) {
+            const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
+#pragma unroll
+            for (int s = 0; s < S; ++s) flush_step<K, false, CK, true>(cx, t4 + s, &ga, s);
+        } else {
+#pragma unroll 1
+            for (int s = 0; s < S; ++s) flush_step<K, true, CK>(cx, t4 + s);
+        }
+    };
+    int i = 0;
+    for (int t4 = t0; t4 < bg.tend; t4 += S, ++i) {
+        if (chain_done < i) {
+            chain_done = wait_progress(pr_chain, i, lane, F);
+            if (chain_done < 0) {
+                cp_wait<0>();
+                return false;
+            }
+        }
+        __syncwarp();
+        flush_group(t4 - S);
+#ifndef FGM_WS_NOLOAD  // (timing probe: no ring loads)
+        if (V4 && t4 >= issue_lo && t4 < issue_hi) {  // (rows outside the image: a clamped row, never read unclamped)
             issue_flat<K>(flat, t4);
         } else {
             issue_row<K, V4>(own, t4, w);
             if (has_x) issue_row<K, V4>(ext, t4, w);
         }
+#endif
         cp_commit();
-        if (lane == 0) st_release_cta(pr_mine, n + 1);  // this warp reads no record of a group <= n - 2 again
+        cp_wait<Gm::M - 1>();
+        __syncwarp();  // every lane's blocks of iteration i - M + 1 have landed
+        if (lane == 0) st_volatile_cta(pr_mine, i + 2);
     }
+    chain_done = wait_progress(pr_chain, i, lane, F);
     cp_wait<0>();
+    if (chain_done < 0) return false;
     __syncwarp();
+    flush_group(t0 + (i - 1) * S);
     return true;
 }
 
-// ---- producer warp -----------------------------------------------------------
+// ---- producer warps -----------------------------------------------------------
 
 template <bool V4>
 __device__ __forceinline__ void put_alpha(const float* g, unsigned srow, int x0, int w, int aw_mask) {
@@ -753,49 +878,96 @@ __device__ __forceinline__ void put_alpha(const float* g, unsigned srow, int x0,
     }
 }
 
-// The record of pixel (x, band row r): alpha ring row r + K, record row
-// r + K - 1.  G: clamp the neighbours at the image border (a clamped
-// neighbour is the pixel itself: edge weight eps, multilevel.cpp:104-106).
-template <int K, bool G, int CK>
-__device__ __forceinline__ void produce_pixel(int r, int x, int y, int w, int h, float eps, float omega) {
+// Store the record of pixel (x, band row r): record row r + K - 1.
+template <int K, int CK>
+__device__ __forceinline__ void store_record(const CoefR& co, float a, int r, int x, bool on) {
     using Gm = Geom<K, CK>;
-#ifdef FGM_WS_NOPROD  // timing probe: the chain warps alone
-    return;
-#endif
-    const int ca = Gm::OFF_AL + (r + K) * Gm::ARS;
-    const int i0 = x & (Gm::AW - 1), im = (x - 1) & (Gm::AW - 1), ip = (x + 1) & (Gm::AW - 1);
-    const float a = lds(ca + i0);
-    float aL = lds(ca + im), aR = lds(ca + ip), aU = lds(ca - Gm::ARS + i0), aD = lds(ca + Gm::ARS + i0);
-    if (G) {
-        if (x <= 0) aL = a;
-        if (x >= w - 1) aR = a;
-        if (y <= 0) aU = a;
-        if (y >= h - 1) aD = a;
-    }
-    const CoefR co = pixel_coefr_dl(a, edge_weight(a, aL, eps, omega), aR, aU, aD, 0.0f, eps, omega);
     const float2 pq = upk2(co.pq);
     const int col = x & (Gm::RW - 1);
     const int ri = 4 * ((r + K - 1) * Gm::RS + col);
     const float4 wa = make_float4(co.dL, co.dD, co.dR, co.dU), wb = make_float4(co.iS, a, pq.x, pq.y);
-    sts4(Gm::REC_A + ri, wa);
-    sts4(Gm::REC_B + ri, wb);
-    if (col < Gm::MIR) {
-        sts4(Gm::REC_A + ri + 4 * Gm::RW, wa);
-        sts4(Gm::REC_B + ri + 4 * Gm::RW, wb);
+    if (on) {
+        sts4(Gm::REC_A + ri, wa);
+        sts4(Gm::REC_B + ri, wb);
+        if (col < Gm::MIR) {
+            sts4(Gm::REC_A + ri + 4 * Gm::RW, wa);
+            sts4(Gm::REC_B + ri + 4 * Gm::RW, wb);
+        }
     }
 }
 
-template <int K, bool V4, int CK>
-__device__ __forceinline__ bool run_producer(const SweepJob& J, int q, int lane, unsigned sbase, float eps, float omega,
-                                             const SweepFail& F) {
+// The records of producer times t4 .. t4 + S - 1.  Lane r computes pixels
+// (t - r, band row r) for the S times t, carrying a and the right edge weight
+// along the row (the left edge weight of a pixel is the right edge weight of
+// its left neighbour: |a - b| is exactly symmetric); K > 1: lane l < S (K - 1)
+// also computes pixel (t4 + l % S - i, band row -i), i = 1 + l / S, once per
+// group.  GX / GY: clamp the column / row neighbours at the image border (a
+// clamped neighbour is the pixel itself: edge weight eps,
+// multilevel.cpp:104-106).  `al`: float index of this producer's alpha ring.
+template <int K, bool GX, bool GY, int CK>
+__device__ __forceinline__ void produce_group(int al, int t4, int lane, int y0, int w, int h, float eps, float omega) {
     using Gm = Geom<K, CK>;
-    const int w = J.w, h = J.h;
-    const int y0 = q * kRows;
-    const int Umax = w + K - 1;
+#ifdef FGM_WS_NOPROD  // timing probe: the chain warps alone
+    return;
+#endif
+    constexpr int AM = Gm::AW - 1;
+    {
+        const int ca = al + (lane + K) * Gm::ARS;
+        const int y = y0 + lane;
+        int x = t4 - lane;
+        float a = lds(ca + (x & AM));
+        float dL = edge_weight(a, lds(ca + ((x - 1) & AM)), eps, omega);
+#pragma unroll
+        for (int s = 0; s < Gm::S; ++s, ++x) {
+            const float an = lds(ca + ((x + 1) & AM));
+            float aR = an, aU = lds(ca - Gm::ARS + (x & AM)), aD = lds(ca + Gm::ARS + (x & AM));
+            if (GX) {
+                if (x <= 0) dL = eps;
+                if (x >= w - 1) aR = a;
+            }
+            if (GY) {
+                if (y <= 0) aU = a;
+                if (y >= h - 1) aD = a;
+            }
+            const CoefR co = pixel_coefr_dl(a, dL, aR, aU, aD, 0.0f, eps, omega);
+            store_record<K, CK>(co, a, lane, x, true);
+            a = an;
+            dL = co.dR;
+        }
+    }
+    if (K > 1) {
+        const bool on = lane < Gm::S * (K - 1);
+        const int i = on ? 1 + lane / Gm::S : 1;
+        const int x = t4 + (lane % Gm::S) - i, y = y0 - i;
+        const int ca = al + (K - i) * Gm::ARS;
+        const float a = lds(ca + (x & AM));
+        float aL = lds(ca + ((x - 1) & AM)), aR = lds(ca + ((x + 1) & AM));
+        float aU = lds(ca - Gm::ARS + (x & AM)), aD = lds(ca + Gm::ARS + (x & AM));
+        if (GX) {
+            if (x <= 0) aL = a;
+            if (x >= w - 1) aR = a;
+        }
+        if (GY) {
+            if (y <= 0) aU = a;
+            if (y >= h - 1) aD = a;
+        }
+        const CoefR co = pixel_coefr_dl(a, edge_weight(a, aL, eps, omega), aR, aU, aD, 0.0f, eps, omega);
+        store_record<K, CK>(co, a, -i, x, on);
+    }
+}
+
+// Producer pw (0 / 1) computes the groups n = pw (mod 2) from its own alpha
+// ring.  Group n may start once every chain warp works on group >= n - kAhead
+// (its record slots were last read in group n - 6).
+template <int K, bool V4, int CK>
+__device__ __forceinline__ bool run_producer(const SweepJob& J, int q, int pw, int lane, unsigned sbase, float eps,
+                                             float omega, const SweepFail& F) {
+    using Gm = Geom<K, CK>;
+    const BandGeo<K, CK> bg(J, q);
+    const int w = bg.w, h = bg.h, y0 = bg.y0;
     constexpr int S = Gm::S;
     constexpr int t0 = -S;
-    const int tend = 31 + Umax;
-    const int ngroups = (tend - t0 + S - 1) / S;
+    const int al = Gm::OFF_AL + pw * Gm::NA * Gm::ARS;
 
     // alpha rows this lane streams: band row `lane` and, lanes 0..K, one of
     // the rows -K..-1, 32
@@ -804,24 +976,29 @@ __device__ __forceinline__ bool run_producer(const SweepJob& J, int q, int lane,
     const int yo = y0 + lane, ye = y0 + er;
     const float* g_own = yo < h ? J.alpha + (long long)yo * J.ipitch : nullptr;
     const float* g_ext = has_e && ye >= 0 && ye < h ? J.alpha + (long long)ye * J.ipitch : nullptr;
-    const unsigned s_own = sbase + 4u * unsigned(Gm::OFF_AL + (lane + K) * Gm::ARS);
-    const unsigned s_ext = sbase + 4u * unsigned(Gm::OFF_AL + (er + K) * Gm::ARS);
-    const unsigned pr_prod = sbase + 4u * unsigned(Gm::OFF_PR);
+    const unsigned s_own = sbase + 4u * unsigned(al + (lane + K) * Gm::ARS);
+    const unsigned s_ext = sbase + 4u * unsigned(al + (er + K) * Gm::ARS);
+    const unsigned pr = sbase + 4u * unsigned(Gm::OFF_PR);
+    const unsigned pr_mine = pr + 4u * unsigned(Gm::PR_PROD + pw);
 
-    for (int x0 = 0; x0 <= ((t0 + Gm::LA - lane) & ~(S - 1)); x0 += S) put_alpha<V4>(g_own, s_own, x0, w, Gm::AW - 1);
-    for (int x0 = 0; x0 <= ((t0 + Gm::LA - er) & ~(S - 1)); x0 += S) put_alpha<V4>(g_ext, s_ext, x0, w, Gm::AW - 1);
+    // an iteration covers 2S producer times: two S-column blocks per row
+    const int tfirst = t0 + pw * S;
+    for (int x0 = 0; x0 <= ((tfirst - S + Gm::LA - lane) & ~(S - 1)); x0 += S) put_alpha<V4>(g_own, s_own, x0, w, Gm::AW - 1);
+    for (int x0 = 0; x0 <= ((tfirst - S + Gm::LA - er) & ~(S - 1)); x0 += S) put_alpha<V4>(g_ext, s_ext, x0, w, Gm::AW - 1);
     cp_commit();
 #pragma unroll
     for (int i = 1; i < Gm::MA; ++i) cp_commit();
 
-    const bool yband = y0 - (K - 1) <= 0 || y0 + 31 >= h - 1;
     int chain_at = 0;  // cached min over the chain warps of their finished groups
-    int n = 0;
-    for (int t4 = t0; n < ngroups; t4 += S, ++n) {
-        if (n - kAhead > chain_at) {  // the slots of group n are read until the chain warps are past group n - 6
+    int it = 0;
+    TR_DECL;
+    for (int n = pw; n < bg.ngroups; n += 2, ++it) {
+        const int t4 = t0 + n * S;
+        TR(0);
+        if (n - kAhead > chain_at) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const int v = wait_progress(pr_prod + 4u * unsigned(1 + c), n - kAhead, lane, F);
+                const int v = wait_progress(pr + 4u * unsigned(Gm::PR_CHAIN + c), n - kAhead, lane, F);
                 if (v < 0) {
                     cp_wait<0>();
                     return false;
@@ -829,29 +1006,39 @@ __device__ __forceinline__ bool run_producer(const SweepJob& J, int q, int lane,
                 chain_at = c == 0 ? v : min(chain_at, v);
             }
         }
+        TR(1);
         cp_wait<Gm::MA - 1>();
         __syncwarp();
-        if (!yband && t4 - 31 >= 1 && t4 + S - 1 <= w - 2) {
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int x = t4 + s - lane;
-                produce_pixel<K, false, CK>(lane, x, y0 + lane, w, h, eps, omega);
-                if (K > 1 && lane >= 1 && lane < K) produce_pixel<K, false, CK>(-lane, x, y0 - lane, w, h, eps, omega);
-            }
-        } else {
-#pragma unroll 1
-            for (int s = 0; s < S; ++s) {
-                const int x = t4 + s - lane;
-                produce_pixel<K, true, CK>(lane, x, y0 + lane, w, h, eps, omega);
-                if (K > 1 && lane >= 1 && lane < K) produce_pixel<K, true, CK>(-lane, x, y0 - lane, w, h, eps, omega);
+        TR(2);
+        const bool xin = t4 - 31 >= 1 && t4 + S - 1 <= w - 2;  // every pixel of the group has both column neighbours
+        if (xin && !bg.yband)
+            produce_group<K, false, false, CK>(al, t4, lane, y0, w, h, eps, omega);
+        else if (xin)
+            produce_group<K, false, true, CK>(al, t4, lane, y0, w, h, eps, omega);
+        else
+            produce_group<K, true, true, CK>(al, t4, lane, y0, w, h, eps, omega);
+        TR(3);
+        __syncwarp();  // every lane's records are issued, every lane's alpha reads are done
+#ifndef FGM_WS_NOLOAD
+        {
+            const int b_own = (t4 + S + Gm::LA - lane) & ~(S - 1), b_ext = (t4 + S + Gm::LA - er) & ~(S - 1);
+            put_alpha<V4>(g_own, s_own, b_own - S, w, Gm::AW - 1);
+            put_alpha<V4>(g_own, s_own, b_own, w, Gm::AW - 1);
+            if (has_e) {
+                put_alpha<V4>(g_ext, s_ext, b_ext - S, w, Gm::AW - 1);
+                put_alpha<V4>(g_ext, s_ext, b_ext, w, Gm::AW - 1);
             }
         }
-        __syncwarp();  // every lane's records are written, every lane's alpha reads are done
-        put_alpha<V4>(g_own, s_own, (t4 + S + Gm::LA - lane) & ~(S - 1), w, Gm::AW - 1);
-        if (has_e) put_alpha<V4>(g_ext, s_ext, (t4 + S + Gm::LA - er) & ~(S - 1), w, Gm::AW - 1);
+#endif
         cp_commit();
-        if (lane == 0) st_release_cta(pr_prod, n + 1);
+        if (lane == 0) st_volatile_cta(pr_mine, it + 1);
+        TR(4);
     }
+#ifdef FGM_WS_TRACE
+    if (lane == 0 && pw == 0 && (q == 0 || q == 1 || q == J.nb / 2))
+        printf("producer %d/%d K=%d iterations %d: total %lld cyc | loop %lld chainwait %lld cpwait %lld produce %lld issue %lld\n",
+               q, J.nb, K, it, clock64() - tr_start, tr_[0], tr_[1], tr_[2], tr_[3], tr_[4]);
+#endif
     cp_wait<0>();
     __syncwarp();
     return true;
@@ -867,17 +1054,24 @@ struct SweepArgs {
     int fault;
 };
 
+// Warp roles of a band CTA: warps 0-2 the chain warps of channels 0-2, warps
+// 4-6 their helpers (a channel's two warps share a scheduler: the helper is
+// light), warps 3 and 7 the producers (the fourth scheduler).
+constexpr int kWsThreads = 256;
+
 template <int K, bool V4, int CK>
 __device__ __forceinline__ void run_band_cta(const SweepJob& J, int q, int warp, int lane, unsigned sbase,
                                              const SweepArgs& A) {
-    if (warp == 0)
-        run_producer<K, V4, CK>(J, q, lane, sbase, A.eps, A.omega, A.fail);
+    if ((warp & 3) == 3)
+        run_producer<K, V4, CK>(J, q, warp >> 2, lane, sbase, A.eps, A.omega, A.fail);
+    else if (warp < 3)
+        run_chain<K, CK>(J, q, warp, lane, sbase, A.fail, A.fault);
     else
-        run_chain<K, V4, CK>(J, q, warp - 1, lane, sbase, A.fail, A.fault);
+        run_helper<K, V4, CK>(J, q, warp - 4, lane, sbase, A.fail, A.fault);
 }
 
 template <int K, int CK>
-__global__ void __launch_bounds__(128, 1) sweep_ws_kernel(SweepArgs A) {
+__global__ void __launch_bounds__(kWsThreads, 1) sweep_ws_kernel(SweepArgs A) {
     using Gm = Geom<K, CK>;
     __shared__ unsigned s_tk;
     const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(ws_sm4));
@@ -888,7 +1082,7 @@ __global__ void __launch_bounds__(128, 1) sweep_ws_kernel(SweepArgs A) {
             if (*reinterpret_cast<volatile int*>(A.fail.abort_flag)) tk = 0xffffffffu;
             s_tk = tk;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) reinterpret_cast<int*>(smf())[Gm::OFF_PR + i] = 0;
+            for (int i = 0; i < Gm::NPR; ++i) reinterpret_cast<int*>(smf())[Gm::OFF_PR + i] = 0;
         }
         __syncthreads();
         const unsigned tk = s_tk;
@@ -918,7 +1112,7 @@ cudaError_t ws_grid_cap(int& cap) {
         int sms = 0, per_sm = 0;
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_ws_kernel<K, kChunk>, 128, size_t(sm16));
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_ws_kernel<K, kChunk>, kWsThreads, size_t(sm16));
         v = std::max(1, sms * std::max(1, per_sm));
         return e;
     });
@@ -933,13 +1127,23 @@ cudaError_t launch_ws_k(const SweepArgs& A, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(A.total_bands, cap));
     if (A.total_bands <= cap)
-        sweep_ws_kernel<K, 4><<<grid, 128, size_t(Geom<K, 4>::TOTAL) * sizeof(float), s>>>(A);
+        sweep_ws_kernel<K, 4><<<grid, kWsThreads, size_t(Geom<K, 4>::TOTAL) * sizeof(float), s>>>(A);
     else
-        sweep_ws_kernel<K, kChunk><<<grid, 128, size_t(Geom<K, kChunk>::TOTAL) * sizeof(float), s>>>(A);
+        sweep_ws_kernel<K, kChunk><<<grid, kWsThreads, size_t(Geom<K, kChunk>::TOTAL) * sizeof(float), s>>>(A);
     return cudaGetLastError();
 }
 
 }  // namespace
+
+cudaError_t ws_band_capacity(int K, int& cap) {
+    switch (K) {
+        case 1: return ws_grid_cap<1>(cap);
+        case 2: return ws_grid_cap<2>(cap);
+        case 3: return ws_grid_cap<3>(cap);
+        case 4: return ws_grid_cap<4>(cap);
+        default: return cudaErrorInvalidValue;
+    }
+}
 
 cudaError_t launch_sweep_ws(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
                             float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s) {
