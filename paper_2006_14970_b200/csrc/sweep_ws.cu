@@ -1,28 +1,37 @@
 // K3, latency path: the warp-specialised sweep kernel for launches of a few
 // images, whose time is the wavefront's dependency chain ((w + h) steps of one
-// lane), not throughput.  One CTA of four warps per 32-row band:
+// lane, plus ~36 steps per band hand-over), not throughput.  One CTA of eight
+// warps per 32-row band:
 //
-//   * warp 0, the producer, computes every pixel's alpha-only coefficients
-//     (the 2x2 matrix is shared by all channels, multilevel.hpp:37-43) ONCE,
-//     ahead of the wavefront, into a shared-memory record ring
-//     {dL, dD, dR, dU | 1/S, a, u0/D, u1/D};
-//   * warps 1-3, the chain warps (one per colour channel), run only the
-//     recurrence of multilevel.cpp:104-118: receive the previous lane's
-//     outputs (shfl), load the records of their K pixels (two LDS.128 each),
-//     apply (pixel_applyr), publish.  A group of four steps is straight-line
-//     code with no barrier inside: output rows are flushed once per group
-//     from a 32-column output ring, so the compiler pipelines across steps.
+//   * two producer warps compute every pixel's alpha-only coefficients (the
+//     2x2 matrix is shared by all channels, multilevel.hpp:37-43) ONCE, ahead
+//     of the wavefront, into a shared-memory record ring
+//     {dL, dD, dR, dU | 1/S, a, u0/D, u1/D} (alternate groups of four steps
+//     each, from their own alpha rings);
+//   * three chain warps (one per colour channel) run only the recurrence of
+//     multilevel.cpp:104-118: receive the previous lane's outputs (shfl), load
+//     the records of their K pixels (two LDS.128 each), apply (pixel_applyr),
+//     store into a 32-column output ring.  A group of four steps is
+//     straight-line code with no barrier, no cp.async and no global store
+//     except lane 31's boundary-stream words;
+//   * three helper warps (one per channel) stream the channel's I_c and initial
+//     F_c / B_c rows into shared-memory rings ahead of the chain warp (cp.async)
+//     and flush its completed 16-column output segments behind it.
 //
-// The producer does not depend on the band above, so a band's coefficients are
-// ready long before its first boundary chunk arrives: the band start, which
-// is on the chain's critical path, costs no coefficient latency.
+// Neither the producers nor the helpers depend on the band above, so a band's
+// coefficients and ring data are in shared memory long before its first
+// boundary chunk arrives: a band start, which is on the chain's critical
+// path, waits for nothing but the chunk.
 //
-// Producer and chain warps synchronise through monotonic progress counters in
-// shared memory (st.release / ld.acquire, cached by the reader): the chain
-// warps start group n once the producer has finished group n + 1, the
-// producer starts group P once every chain warp works on group >= P - 4
-// (record slots are reused after 32 columns = 8 groups).  Every wait is
-// bounded (the launch's abort flag and spin timeout).
+// The warps synchronise through monotonic progress counters in shared memory
+// (volatile, cached by the reader; see st_volatile_cta): a chain warp starts
+// group n once its helper has published the group's ring data and the
+// producers have finished groups n and n + 1; a producer starts group P once
+// every chain warp works on group >= P - 4 (record slots are reused after 32
+// columns = 8 groups); a helper runs iteration i (flush group i - 1, issue the
+// blocks that overwrite columns last read in group i - 1) once its chain warp
+// has finished group i - 1.  Every wait is bounded (the launch's abort flag
+// and spin timeout).
 //
 // Geometry, boundary streams, ticket order and border handling are those of
 // lane j of a chain warp owns skewed row v = 32q + j and
@@ -31,6 +40,9 @@
 // words, no fences), lane 31 publishes this band's.  The arithmetic is
 // pixel_coefr_dl / pixel_applyr of fgm_device.cuh, operation for operation:
 // results are bitwise those of the throughput kernel (sweep.cu).
+//
+// -DFGM_WS_TRACE: per-phase cycle counts and a band timeline (printf) for
+// development; profiles/r02/k3_ws_notes.txt.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -284,16 +296,19 @@ __device__ __forceinline__ FlatSrc<K> make_flat(const SweepJob& J, int ch, int y
     return f;
 }
 
-template <int K>
+// LO: a band's first groups, where the blocks of the lower rows are still left
+// of column 0 (skipped).
+template <int K, bool LO = false>
 __device__ __forceinline__ void issue_flat(const FlatSrc<K>& f, int t4) {
     using G = Geom<K>;
 #pragma unroll
     for (int i = 0; i < FlatSrc<K>::N; ++i) {
-        const unsigned x0 = unsigned(t4 + f.q[i]) & ~unsigned(G::S - 1);
+        const int xs = (t4 + f.q[i]) & ~(G::S - 1);
+        const unsigned x0 = unsigned(LO ? max(xs, 0) : xs);
         const unsigned c = x0 & (G::RW - 1);
         const float* g = f.g[i] + x0;
         const unsigned d = f.s[i] + 4u * c;
-        const unsigned on = (f.on >> i) & 1u;
+        const unsigned on = (f.on >> i) & (LO ? (xs >= 0 ? 1u : 0u) : 1u);
         cp_async16_if(d, g, on);
         cp_async16_if(d + 4u * G::RW, g, on & (c < unsigned(G::MIR) ? 1u : 0u));
     }
@@ -353,7 +368,7 @@ __device__ __forceinline__ bool acquire_chunk(float4 v, const float* up_stream, 
     const bool mine = lane < G::CH4 && 4 * lane < nvalid;
     unsigned long long t0 = 0;
     for (unsigned n = 0; !__all_sync(kFull, chunk_complete<K, CK>(v, u0, Umax, lane)); ++n) {
-        __nanosleep(32);
+        if (CK > 4) __nanosleep(32);  // (4-column chunks: latency-bound launches, the load's round trip is the poll interval)
         if (mine) v = ld_relaxed_v4(up_stream + size_t(u0) * K * 2 + 4 * lane);
         if (!keep_waiting(n, t0, lane, F)) return false;
     }
@@ -699,8 +714,18 @@ __device__ __forceinline__ bool run_chain(const SweepJob& J, int q, int ch, int 
     int loaded = 0;            // cached helper progress (groups whose ring data is in shared memory)
     int n = 0;
     TR_DECL;
+#ifdef FGM_WS_TRACE
+    unsigned long long tl_[6] = {global_ns(), 0, 0, 0, 0, 0};
+#endif
     for (int t4 = t0; t4 < bg.tend; t4 += S, ++n) {
         TR(0);
+#ifdef FGM_WS_TRACE
+        if (n == 1) tl_[1] = global_ns();   // before group t4 = 0
+        if (n == 2) tl_[2] = global_ns();   // after group t4 = 0
+        if (n == 10) tl_[3] = global_ns();  // after step 35
+        if (n == 100) tl_[4] = global_ns();
+        if (n == 200) tl_[5] = global_ns();
+#endif
         if (loaded < n + 1) {
             loaded = wait_progress(pr_load, n + 1, lane, F);
             if (loaded < 0) return false;
@@ -773,6 +798,9 @@ __device__ __forceinline__ bool run_chain(const SweepJob& J, int q, int ch, int 
         TR(5);
     }
 #ifdef FGM_WS_TRACE
+    if (lane == 0 && ch == 0 && (q <= 3 || q == J.nb / 2))
+        printf("timeline band %d: launch +0, before g0 %llu ns, after g0 %llu, after step 35 %llu, n=100 %llu, n=200 %llu, end %llu\n", q,
+               tl_[1] - tl_[0], tl_[2] - tl_[0], tl_[3] - tl_[0], tl_[4] - tl_[0], tl_[5] - tl_[0], global_ns() - tl_[0]);
     if (lane == 0 && ch == 0 && (q == 0 || q == 1 || q == J.nb / 2 || q == J.nb - 1))
         printf("chain %d/%d K=%d w=%d groups %d: total %lld cyc | loop %lld loadwait %lld prodwait %lld chunk %lld steps %lld "
                "publish %lld\n",
@@ -826,6 +854,10 @@ __device__ __forceinline__ bool run_helper(const SweepJob& J, int q, int ch, int
             const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
 #pragma unroll
             for (int s = 0; s < S; ++s) flush_step<K, false, CK, true>(cx, t4 + s, &ga, s);
+        } else if (t4 < bg.fast_lo && t4 + S <= bg.fast_hi) {  // band start: segments left of column 0 are skipped
+            const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
+#pragma unroll
+            for (int s = 0; s < S; ++s) flush_step<K, false, CK, true, true>(cx, t4 + s, &ga, s);
         } else {
 #pragma unroll 1
             for (int s = 0; s < S; ++s) flush_step<K, true, CK>(cx, t4 + s);
@@ -842,14 +874,14 @@ __device__ __forceinline__ bool run_helper(const SweepJob& J, int q, int ch, int
         }
         __syncwarp();
         flush_group(t4 - S);
-#ifndef FGM_WS_NOLOAD  // (timing probe: no ring loads)
         if (V4 && t4 >= issue_lo && t4 < issue_hi) {  // (rows outside the image: a clamped row, never read unclamped)
             issue_flat<K>(flat, t4);
+        } else if (V4 && t4 < issue_hi) {  // the band's first groups: every band's start is on the critical path
+            issue_flat<K, true>(flat, t4);
         } else {
             issue_row<K, V4>(own, t4, w);
             if (has_x) issue_row<K, V4>(ext, t4, w);
         }
-#endif
         cp_commit();
         cp_wait<Gm::M - 1>();
         __syncwarp();  // every lane's blocks of iteration i - M + 1 have landed
@@ -907,9 +939,6 @@ __device__ __forceinline__ void store_record(const CoefR& co, float a, int r, in
 template <int K, bool GX, bool GY, int CK>
 __device__ __forceinline__ void produce_group(int al, int t4, int lane, int y0, int w, int h, float eps, float omega) {
     using Gm = Geom<K, CK>;
-#ifdef FGM_WS_NOPROD  // timing probe: the chain warps alone
-    return;
-#endif
     constexpr int AM = Gm::AW - 1;
     {
         const int ca = al + (lane + K) * Gm::ARS;
@@ -1019,7 +1048,6 @@ __device__ __forceinline__ bool run_producer(const SweepJob& J, int q, int pw, i
             produce_group<K, true, true, CK>(al, t4, lane, y0, w, h, eps, omega);
         TR(3);
         __syncwarp();  // every lane's records are issued, every lane's alpha reads are done
-#ifndef FGM_WS_NOLOAD
         {
             const int b_own = (t4 + S + Gm::LA - lane) & ~(S - 1), b_ext = (t4 + S + Gm::LA - er) & ~(S - 1);
             put_alpha<V4>(g_own, s_own, b_own - S, w, Gm::AW - 1);
@@ -1029,7 +1057,6 @@ __device__ __forceinline__ bool run_producer(const SweepJob& J, int q, int pw, i
                 put_alpha<V4>(g_ext, s_ext, b_ext, w, Gm::AW - 1);
             }
         }
-#endif
         cp_commit();
         if (lane == 0) st_volatile_cta(pr_mine, it + 1);
         TR(4);
@@ -1054,20 +1081,22 @@ struct SweepArgs {
     int fault;
 };
 
-// Warp roles of a band CTA: warps 0-2 the chain warps of channels 0-2, warps
-// 4-6 their helpers (a channel's two warps share a scheduler: the helper is
-// light), warps 3 and 7 the producers (the fourth scheduler).
+// Warp roles of a band CTA.  Schedulers serve warp w % 4 and prefer the higher
+// warp id: warps 5-7 are the chain warps of channels 0-2 (one scheduler each,
+// with priority), warps 1-3 their helpers on the same schedulers (they fill
+// the chain warps' stall slots), warps 0 and 4 the producers (the fourth
+// scheduler).
 constexpr int kWsThreads = 256;
 
 template <int K, bool V4, int CK>
 __device__ __forceinline__ void run_band_cta(const SweepJob& J, int q, int warp, int lane, unsigned sbase,
                                              const SweepArgs& A) {
-    if ((warp & 3) == 3)
+    if ((warp & 3) == 0)
         run_producer<K, V4, CK>(J, q, warp >> 2, lane, sbase, A.eps, A.omega, A.fail);
-    else if (warp < 3)
-        run_chain<K, CK>(J, q, warp, lane, sbase, A.fail, A.fault);
+    else if (warp > 4)
+        run_chain<K, CK>(J, q, warp - 5, lane, sbase, A.fail, A.fault);
     else
-        run_helper<K, V4, CK>(J, q, warp - 4, lane, sbase, A.fail, A.fault);
+        run_helper<K, V4, CK>(J, q, warp - 1, lane, sbase, A.fail, A.fault);
 }
 
 template <int K, int CK>

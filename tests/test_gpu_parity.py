@@ -183,6 +183,26 @@ def test_sweep_passes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, K, kernel):
     assert_close("bg", gb.double().cpu().numpy(), ob, tol_max=2e-5, tol_mean=1e-6)
 
 
+# The three K3 kernels run the same operations in the same order
+# (pixel_coefr_dl / pixel_applyr): a single-level pass is bitwise the same
+# whichever one a launch is given (batch == single relies on it).
+@pytest.mark.parametrize("w,h,iters", [(64, 40, 1), (200, 136, 2), (37, 95, 2), (333, 129, 3), (257, 260, 4),
+                                       (1000, 700, 6), (1920, 1080, 2), (33, 33, 2), (4, 70, 2), (70, 4, 4),
+                                       (2050, 70, 2)])
+def test_sweep_kernels_bitwise_equal(fgm, cuda, w, h, iters):
+    g = torch.Generator(device=cuda).manual_seed(w * 7 + h)
+    img = torch.rand((3, h, w), device=cuda, generator=g)
+    a = torch.rand((h, w), device=cuda, generator=g)
+    f0 = torch.rand((3, h, w), device=cuda, generator=g)
+    b0 = torch.rand((3, h, w), device=cuda, generator=g)
+    p = fgm.BASELINE_PARAMS
+    ref = fgm.sweep_passes_cuda(img, a, f0, b0, iters, p.eps_r, p.omega, 2)
+    for kernel in (1, 3):
+        out = fgm.sweep_passes_cuda(img, a, f0, b0, iters, p.eps_r, p.omega, kernel)
+        torch.cuda.synchronize()
+        assert torch.equal(out[0], ref[0]) and torch.equal(out[1], ref[1]), f"kernel {kernel} differs from kernel 2"
+
+
 # ---- resize kernel: image.cpp:71-133, test_image.cpp:88-121 --------------------
 def test_resize_golden_row_bitwise(fgm, cuda):
     out = fgm.resize_cuda(dev(np.array([[[0.0, 1.0]]]), cuda), 4, 1)
@@ -561,7 +581,8 @@ def test_random_sizes_and_params_vs_oracle(fgm, cuda, orc, oracle_mod, seed):
 
 # ---- failure detection: a stalled band hand-over is an error, not a hang ----
 @pytest.mark.gpu
-def test_stalled_handover_returns_runtime_error(fgm, cuda):
+@pytest.mark.parametrize("lat_kernel", [3, 1])
+def test_stalled_handover_returns_runtime_error(fgm, cuda, lat_kernel):
     """SURVEY.md section 5 ("timeout -> error, not a hang"): with band 0 of every
     sweep made to skip publishing its boundary stream (fgm_debug_fault(1)), band
     1 waits for data that never comes; the bounded wait aborts the launch, counts
@@ -571,6 +592,7 @@ def test_stalled_handover_returns_runtime_error(fgm, cuda):
     img, a = synth.make_composite(300, 200, 4242, 4, 3.0)  # 7 bands at the top level
     fgm.device_faults(reset=True)
     fgm.set_spin_timeout_ms(100)
+    fgm.set_latency_kernel(lat_kernel)  # a single image: latency-bound launches (sweep_ws.cu: 3, sweep_lat.cu: 1)
     fgm.debug_fault(1)
     try:
         with pytest.raises(RuntimeError, match="timed out"):
@@ -586,6 +608,7 @@ def test_stalled_handover_returns_runtime_error(fgm, cuda):
                                         **fgm.BASELINE_PARAMS.kwargs())
     assert np.isfinite(f).all() and np.isfinite(b).all()
     assert fgm.device_faults() == 0
+    fgm.set_latency_kernel(3)
 
 
 # ---- the K = 4 throughput sweep (16-column chunks) against the oracle -------
