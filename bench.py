@@ -238,7 +238,7 @@ def time_configs(fgm, synth, torch, dev, peak):
                          "ms_per_solve": round(med, 4), "mp_per_s": round(mp / (med / 1e3), 1),
                          "k3_ms": round(k3_ms, 4), "k3_gbs": round(achieved, 1),
                          "k3_roofline_frac": round(achieved / peak, 4), "reps": reps,
-                         "k3_kernel": "latency kernel (sweep_lat.cu, 32-row bands): a single image is chain-bound"}
+                         "k3_kernel": "latency kernel (sweep_ws.cu: one warp-specialised CTA per 32-row band): a single image is chain-bound"}
         del img, a, fg, bg
         torch.cuda.empty_cache()
     return out

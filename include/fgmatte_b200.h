@@ -136,9 +136,8 @@ int fgm_sweep_passes_f32(const float* image, const float* alpha, const float* fg
                          float* bg_out, void* stream);
 /* The same with the sweep kernel chosen explicitly (parity tests of both):
  * 0 automatic (as fgm_sweep_passes_f32: one image is a latency-bound launch),
- * 1 the latency kernel (32-row bands, one row per lane), 2 the throughput
- * kernel (64-row bands, two rows per lane) that solves batches, 3 the
- * warp-specialised latency kernel (one CTA per 32-row band). */
+ * 1 the latency kernel (one warp-specialised CTA per 32-row band), 2 the throughput
+ * kernel (64-row bands, two rows per lane) that solves batches. */
 int fgm_sweep_passes_kernel_f32(const float* image, const float* alpha, const float* fg_in, const float* bg_in,
                                 int w, int h, int iterations, double regularization, double gradient_weight,
                                 float* fg_out, float* bg_out, int kernel, void* stream);
@@ -148,12 +147,6 @@ int fgm_sweep_passes_kernel_f32(const float* image, const float* alpha, const fl
  * (default) with one resample launch per level (image.cpp:114-133 each).  Both
  * are bitwise identical. */
 void fgm_set_pyramid_mode(int fused);
-
-/* Tuning/debug (process-wide, atomic): the kernel that runs latency-bound
- * sweep launches (<= 4 images): 3 (default) the warp-specialised band CTA
- * (producer warp + one chain warp per channel), 1 the one-warp-per-(band,
- * channel) kernel.  Both are bitwise identical. */
-void fgm_set_latency_kernel(int kernel);
 
 /* Failure detection.  A big-level sweep band waits for the band above
  * through a boundary stream; every such wait is bounded (default 2000 ms,

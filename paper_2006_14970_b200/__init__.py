@@ -120,8 +120,6 @@ def _load():
     L.fgm_profile_enable.argtypes = [C.c_int]
     L.fgm_set_pyramid_mode.argtypes = [C.c_int]
     L.fgm_set_debug_guards.argtypes = [C.c_int]
-    L.fgm_set_latency_kernel.argtypes = [C.c_int]
-    L.fgm_set_latency_kernel.restype = None
     for name in ("fgm_debug_fault", "fgm_set_spin_timeout_ms", "fgm_device_faults"):
         if hasattr(L, name):  # (absent from older builds loaded through FGMATTE_B200_LIB by tools/)
             getattr(L, name).argtypes = [C.c_int]
@@ -148,12 +146,6 @@ def device_count() -> int:
 def set_pyramid_mode(fused: int) -> None:
     """1 fused I/alpha pyramid, 0 (default) one resample launch per level."""
     _load().fgm_set_pyramid_mode(int(fused))
-
-
-def set_latency_kernel(kernel: int) -> None:
-    """Kernel of latency-bound sweep launches (<= 4 images): 3 (default) the
-    warp-specialised band CTA (sweep_ws.cu), 1 one warp per (band, channel)."""
-    _load().fgm_set_latency_kernel(int(kernel))
 
 
 def set_debug_guards(on: int) -> None:
@@ -532,8 +524,7 @@ def compose_cuda(fg, bg, alpha, out=None):
 
 def sweep_passes_cuda(image, alpha, fg, bg, iterations: int, eps_r: float, omega: float, kernel: int = 0):
     """`iterations` exact Gauss-Seidel sweeps of one level (multilevel.cpp:81-121).
-    kernel: 0 automatic, 1 latency kernel (32-row bands), 3 warp-specialised latency
-    kernel, 2 throughput kernel
+    kernel: 0 automatic, 1 latency kernel (one warp-specialised CTA per 32-row band), 2 throughput kernel
     (64-row bands, the one that solves batches)."""
     import torch
 

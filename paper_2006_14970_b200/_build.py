@@ -13,7 +13,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfgmatte_b200.so")
-SOURCES = ["kernels.cu", "sweep.cu", "sweep_lat.cu", "sweep_ws.cu", "solver.cu"]
+SOURCES = ["kernels.cu", "sweep.cu", "sweep_ws.cu", "solver.cu"]
 HEADERS = ["fgm_device.cuh", "fgm_internal.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

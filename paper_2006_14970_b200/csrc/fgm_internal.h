@@ -93,7 +93,7 @@ struct CoarseJob {
 
 // ---- K3: big-level sweep, skewed-band wavefront ---------------------------
 constexpr int kBandRows = 64;     // throughput kernel (sweep.cu): one warp = 64 skewed rows, two per lane
-constexpr int kLatBandRows = 32;  // latency kernel (sweep_lat.cu): one warp = 32 skewed rows, one per lane
+constexpr int kLatBandRows = 32;  // latency kernel (sweep_ws.cu): one CTA = 32 skewed rows, one per lane of a chain warp
 constexpr int kLatMaxJobs = 4;    // launches of at most this many images are chain-bound: latency kernel
 #ifndef FGM_CHUNK
 #define FGM_CHUNK 16
@@ -154,15 +154,11 @@ cudaError_t launch_coarse(const CoarseJob* jobs_dev, int njobs, double eps, doub
 // fault_count: a persistent per-device counter of timed-out waits.
 cudaError_t launch_sweep(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
                          float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
-// The same for jobs cut into kLatBandRows-row bands (the latency kernel,
-// sweep_lat.cu).
-cudaError_t launch_sweep_lat(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
-                             float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
-// The warp-specialised latency kernel (sweep_ws.cu): one CTA per 32-row band,
-// a producer warp computing the alpha-only coefficients once per pixel and one
-// chain warp per channel running the recurrence.  Same jobs, order and streams.
-// ws_band_capacity(): band CTAs resident at once on the current device.
-cudaError_t ws_band_capacity(int K, int& cap);
+// The same for jobs cut into kLatBandRows-row bands: the warp-specialised
+// latency kernel (sweep_ws.cu), one CTA per band -- two producer warps compute
+// the alpha-only coefficients once per pixel, one chain warp per channel runs
+// the recurrence, one helper warp per channel streams the rings and flushes
+// the outputs.  Same jobs, order and streams (three items per band).
 cudaError_t launch_sweep_ws(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
                             float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s);
 extern std::atomic<int> g_sweep_fault;            // debug fault injection (fgm_debug_fault)

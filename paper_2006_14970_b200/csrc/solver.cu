@@ -483,23 +483,10 @@ int read_faults() {
 
 // ticket[0]: the launch's band ticket, ticket[1]: its abort flag (both zeroed)
 // lat: the jobs are cut into kLatBandRows-row bands for the latency kernel
-// Which kernel runs latency-bound launches: 1 the one-warp-per-(band, channel)
-// kernel (sweep_lat.cu), 3 the warp-specialised band CTA (sweep_ws.cu).
-std::atomic<int> g_lat_kernel{3};
-
 cudaError_t launch_sweep_passes(int K, const SweepJob* jd, const int2* od, int bands, unsigned* ticket, float eps,
-                                float omega, bool lat, cudaStream_t s, int lat_kernel = 0) {
-    if (lat && !lat_kernel) {
-        // automatic: the band CTAs of the warp-specialised kernel hold one band
-        // per SM; a launch with more than two rounds of bands (a 16384^2 level)
-        // is bound by resident bands, where the one-warp kernel's 9 warps per
-        // SM win (measured, profiles/r02/k3_ws_notes.txt)
-        lat_kernel = g_lat_kernel.load();
-        int cap = 0;
-        if (lat_kernel == 3 && ws_band_capacity(K, cap) == cudaSuccess && bands > 2 * cap) lat_kernel = 1;
-    }
-    auto fn = !lat ? launch_sweep : lat_kernel == 3 ? launch_sweep_ws : launch_sweep_lat;
-    return fn(K, jd, od, 3 * bands, ticket, eps, omega, reinterpret_cast<int*>(ticket + 1), device_fault_counter(), s);
+                                float omega, bool lat, cudaStream_t s) {
+    return (lat ? launch_sweep_ws : launch_sweep)(K, jd, od, 3 * bands, ticket, eps, omega,
+                                                  reinterpret_cast<int*>(ticket + 1), device_fault_counter(), s);
 }
 
 enum LaunchKind { kCoarse, kResample, kUpsample, kSweep, kCopy, kPyramid };
@@ -1320,7 +1307,7 @@ int fgm_sweep_passes_kernel_f32(const float* image, const float* alpha, const fl
     return guarded([&] {
         check_dims(w, h);
         if (iterations < 1) throw InvalidArgument("MlParams: iteration counts must be >= 1");
-        if (kernel < 0 || kernel > 3) throw InvalidArgument("sweep kernel must be 0 (automatic), 1, 2 or 3");
+        if (kernel < 0 || kernel > 2) throw InvalidArgument("sweep kernel must be 0 (automatic), 1 or 2");
         const bool lat = kernel != 2;  // one image: latency-bound
         const int rows = lat ? kLatBandRows : kBandRows;
         fgm_params p{regularization, gradient_weight, 1, 1, 1};
@@ -1371,7 +1358,7 @@ int fgm_sweep_passes_kernel_f32(const float* image, const float* alpha, const fl
             {
                 ProfScope pr(s, 0, 64.0 * double(px));
                 ck(launch_sweep_passes(ps[pi], d, dord, J1.nb, ctr, float(regularization), float(gradient_weight), lat,
-                                       s, kernel == 1 || kernel == 3 ? kernel : 0),
+                                       s),
                    "sweep_kernel");
             }
             fi = J1.fg_out;
@@ -1382,7 +1369,6 @@ int fgm_sweep_passes_kernel_f32(const float* image, const float* alpha, const fl
 
 void fgm_debug_fault(int code) { fgm::g_sweep_fault.store(code); }
 
-void fgm_set_latency_kernel(int kernel) { fgm::g_lat_kernel.store(kernel == 1 ? 1 : 3); }
 
 void fgm_set_spin_timeout_ms(int ms) { fgm::g_spin_timeout_ns.store((long long)std::max(ms, 1) * 1000000ll); }
 

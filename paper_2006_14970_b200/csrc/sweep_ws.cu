@@ -1164,16 +1164,6 @@ cudaError_t launch_ws_k(const SweepArgs& A, cudaStream_t s) {
 
 }  // namespace
 
-cudaError_t ws_band_capacity(int K, int& cap) {
-    switch (K) {
-        case 1: return ws_grid_cap<1>(cap);
-        case 2: return ws_grid_cap<2>(cap);
-        case 3: return ws_grid_cap<3>(cap);
-        case 4: return ws_grid_cap<4>(cap);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
 cudaError_t launch_sweep_ws(int K, const SweepJob* jobs_dev, const int2* order_dev, int total_items, unsigned* ticket,
                             float eps, float omega, int* abort_flag, int* fault_count, cudaStream_t s) {
     SweepArgs A;

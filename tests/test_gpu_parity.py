@@ -75,12 +75,12 @@ def test_ml_vs_oracle_params(fgm, cuda, orc, oracle_mod, kw):
     assert_close("bg", b, ob)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("kernel", [1, 2])
 @pytest.mark.parametrize("w,h", [(7, 100), (37, 65), (39, 200), (40, 33), (41, 31), (64, 97), (300, 32), (300, 33),
                                  (90, 130), (200, 129), (123, 64), (96, 66)])
 def test_sweep_border_modes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, kernel):
     # narrow levels and bands at the row borders: the border / row-border /
-    # band-start variants of the K3 kernels (sweep_lat.cu: 1, sweep.cu: 2, sweep_ws.cu: 3)
+    # band-start variants of both K3 kernels (sweep_ws.cu: 1, sweep.cu: 2)
     # against the fp64 oracle, level by level through the single-level entry
     # (BASELINE params, K = 1..4)
     rng = np.random.default_rng(w * 1000 + h)
@@ -163,7 +163,7 @@ def test_coarse_levels_bitwise_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, param
 
 
 # ---- single level: K fused sweeps vs `iterations` oracle sweeps ---------------
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("kernel", [1, 2])
 @pytest.mark.parametrize("w,h,K", [(37, 29, 1), (64, 64, 2), (100, 70, 3), (130, 97, 4), (50, 40, 8), (33, 200, 10),
                                    (1, 50, 2), (50, 1, 2), (300, 33, 2), (257, 129, 2), (700, 300, 2), (520, 260, 4),
                                    (333, 190, 1)])
@@ -183,7 +183,7 @@ def test_sweep_passes_vs_oracle(fgm, cuda, orc, oracle_mod, w, h, K, kernel):
     assert_close("bg", gb.double().cpu().numpy(), ob, tol_max=2e-5, tol_mean=1e-6)
 
 
-# The three K3 kernels run the same operations in the same order
+# Both K3 kernels run the same operations in the same order
 # (pixel_coefr_dl / pixel_applyr): a single-level pass is bitwise the same
 # whichever one a launch is given (batch == single relies on it).
 @pytest.mark.parametrize("w,h,iters", [(64, 40, 1), (200, 136, 2), (37, 95, 2), (333, 129, 3), (257, 260, 4),
@@ -197,10 +197,9 @@ def test_sweep_kernels_bitwise_equal(fgm, cuda, w, h, iters):
     b0 = torch.rand((3, h, w), device=cuda, generator=g)
     p = fgm.BASELINE_PARAMS
     ref = fgm.sweep_passes_cuda(img, a, f0, b0, iters, p.eps_r, p.omega, 2)
-    for kernel in (1, 3):
-        out = fgm.sweep_passes_cuda(img, a, f0, b0, iters, p.eps_r, p.omega, kernel)
-        torch.cuda.synchronize()
-        assert torch.equal(out[0], ref[0]) and torch.equal(out[1], ref[1]), f"kernel {kernel} differs from kernel 2"
+    out = fgm.sweep_passes_cuda(img, a, f0, b0, iters, p.eps_r, p.omega, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(out[0], ref[0]) and torch.equal(out[1], ref[1]), "the latency kernel differs from the throughput kernel"
 
 
 # ---- resize kernel: image.cpp:71-133, test_image.cpp:88-121 --------------------
@@ -581,8 +580,7 @@ def test_random_sizes_and_params_vs_oracle(fgm, cuda, orc, oracle_mod, seed):
 
 # ---- failure detection: a stalled band hand-over is an error, not a hang ----
 @pytest.mark.gpu
-@pytest.mark.parametrize("lat_kernel", [3, 1])
-def test_stalled_handover_returns_runtime_error(fgm, cuda, lat_kernel):
+def test_stalled_handover_returns_runtime_error(fgm, cuda):
     """SURVEY.md section 5 ("timeout -> error, not a hang"): with band 0 of every
     sweep made to skip publishing its boundary stream (fgm_debug_fault(1)), band
     1 waits for data that never comes; the bounded wait aborts the launch, counts
@@ -592,7 +590,6 @@ def test_stalled_handover_returns_runtime_error(fgm, cuda, lat_kernel):
     img, a = synth.make_composite(300, 200, 4242, 4, 3.0)  # 7 bands at the top level
     fgm.device_faults(reset=True)
     fgm.set_spin_timeout_ms(100)
-    fgm.set_latency_kernel(lat_kernel)  # a single image: latency-bound launches (sweep_ws.cu: 3, sweep_lat.cu: 1)
     fgm.debug_fault(1)
     try:
         with pytest.raises(RuntimeError, match="timed out"):
@@ -608,7 +605,6 @@ def test_stalled_handover_returns_runtime_error(fgm, cuda, lat_kernel):
                                         **fgm.BASELINE_PARAMS.kwargs())
     assert np.isfinite(f).all() and np.isfinite(b).all()
     assert fgm.device_faults() == 0
-    fgm.set_latency_kernel(3)
 
 
 # ---- the K = 4 throughput sweep (16-column chunks) against the oracle -------

@@ -1,5 +1,5 @@
 """Device time of one single-level pass of each K3 kernel (1 latency, 2
-throughput, 3 warp-specialised latency) on single images of the BASELINE sizes (development aid: the
+throughput) on single images of the BASELINE sizes (development aid: the
 kernel choice per launch shape; profiles/r02/k3_v2_notes.txt)."""
 import sys
 
@@ -17,7 +17,7 @@ for (w, h, iters) in [(512, 512, 2), (1920, 1080, 2), (4096, 4096, 2), (8192, 81
     f0 = torch.rand((3, h, w), device="cuda", generator=g)
     b0 = torch.rand((3, h, w), device="cuda", generator=g)
     res = []
-    for kern in (1, 2, 3):
+    for kern in (1, 2):
         for _ in range(2):
             fgm.sweep_passes_cuda(img, a, f0, b0, iters, p.eps_r, p.omega, kern)
         torch.cuda.synchronize()
@@ -29,6 +29,6 @@ for (w, h, iters) in [(512, 512, 2), (1920, 1080, 2), (4096, 4096, 2), (8192, 81
         e1.record()
         torch.cuda.synchronize()
         res.append(e0.elapsed_time(e1) / n)
-    print(f"{w}x{h} K={iters}: latency {res[0]:.3f} ms  throughput {res[1]:.3f} ms  warp-specialised {res[2]:.3f} ms", flush=True)
+    print(f"{w}x{h} K={iters}: latency {res[0]:.3f} ms  throughput {res[1]:.3f} ms", flush=True)
     del img, a, f0, b0
     torch.cuda.empty_cache()
