@@ -421,6 +421,28 @@ def test_batch_equals_single_bitwise(fgm, cuda):
         assert torch.equal(f, f1) and torch.equal(b, b1)
 
 
+def test_small_batch_latency_launches_bitwise_and_vs_oracle(fgm, cuda, orc, oracle_mod):
+    # a batch of <= 4 images: every big-level launch is latency-bound and runs the
+    # warp-specialised kernel (sweep_ws.cu) with the bands of several jobs in
+    # one ticket order; bitwise the single solves, and the oracle within tolerance
+    from paper_2006_14970_b200 import synth
+
+    sizes = [(640, 410), (333, 500), (97, 1100)]
+    imgs, alps = [], []
+    for i, (w, h) in enumerate(sizes):
+        im, al = synth.make_composite(w, h, 990 + i, 4, 3.0)
+        imgs.append(im)
+        alps.append(al)
+    p = oracle_mod.Params()
+    outs = fgm.batch_solve_cuda([x.to(cuda) for x in imgs], [x.to(cuda) for x in alps], params_from(fgm, p))
+    for im, al, (f, b) in zip(imgs, alps, outs):
+        f1, b1 = fgm.ml_foreground_background_cuda(im.to(cuda), al.to(cuda), params_from(fgm, p))
+        assert torch.equal(f, f1) and torch.equal(b, b1)
+        of, ob = orc.ml_solve(im.double().numpy(), al.double().numpy(), p)
+        assert_close("fg", f.double().cpu().numpy(), of)
+        assert_close("bg", b.double().cpu().numpy(), ob)
+
+
 def test_fused_pyramid_bitwise(fgm, cuda):
     # one pass over the full-res input for every level's I/alpha (pyramid_kernel)
     # == one resample launch per level (image.cpp:114-133): same taps, same
