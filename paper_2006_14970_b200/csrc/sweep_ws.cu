@@ -811,11 +811,12 @@ __device__ __forceinline__ bool run_chain(const SweepJob& J, int q, int ch, int 
 
 // Helper warp of channel ch: streams the channel's I_c / F_c / B_c rows into
 // the rings ahead of the chain warp and flushes its output rows behind it.
-// Iteration i runs once the chain warp has finished group i - 1: it flushes
-// that group's completed output segments, issues the ring blocks "of the end
-// of group i" (they overwrite columns last read in group i - 1), and, after
-// waiting for the blocks issued M - 1 iterations earlier, publishes the ring
-// data of chain group i + 1.
+// Iteration i first publishes the ring data of chain group i + 1 (the blocks
+// issued M - 1 iterations earlier have landed: nothing the chain warp waits
+// for depends on the rest of the iteration); then, once the chain warp has
+// finished group i - 1, it issues the ring blocks "of the end of group i" (they
+// overwrite columns last read in group i - 1) and flushes group i - 1's
+// completed output segments.
 template <int K, bool V4, int CK>
 __device__ __forceinline__ bool run_helper(const SweepJob& J, int q, int ch, int lane, unsigned sbase, const SweepFail& F,
                                            int fault) {
@@ -865,6 +866,11 @@ __device__ __forceinline__ bool run_helper(const SweepJob& J, int q, int ch, int
     };
     int i = 0;
     for (int t4 = t0; t4 < bg.tend; t4 += S, ++i) {
+        // first, what the chain warp may be waiting for: the blocks issued M - 1
+        // iterations ago have landed -- the ring data of chain group i + 1
+        cp_wait<Gm::M - 2>();
+        __syncwarp();
+        if (lane == 0) st_volatile_cta(pr_mine, i + 2);
         if (chain_done < i) {
             chain_done = wait_progress(pr_chain, i, lane, F);
             if (chain_done < 0) {
@@ -873,7 +879,6 @@ __device__ __forceinline__ bool run_helper(const SweepJob& J, int q, int ch, int
             }
         }
         __syncwarp();
-        flush_group(t4 - S);
         if (V4 && t4 >= issue_lo && t4 < issue_hi) {  // (rows outside the image: a clamped row, never read unclamped)
             issue_flat<K>(flat, t4);
         } else if (V4 && t4 < issue_hi) {  // the band's first groups: every band's start is on the critical path
@@ -883,9 +888,7 @@ __device__ __forceinline__ bool run_helper(const SweepJob& J, int q, int ch, int
             if (has_x) issue_row<K, V4>(ext, t4, w);
         }
         cp_commit();
-        cp_wait<Gm::M - 1>();
-        __syncwarp();  // every lane's blocks of iteration i - M + 1 have landed
-        if (lane == 0) st_volatile_cta(pr_mine, i + 2);
+        flush_group(t4 - S);
     }
     chain_done = wait_progress(pr_chain, i, lane, F);
     cp_wait<0>();
