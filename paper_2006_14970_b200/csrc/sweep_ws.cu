@@ -330,8 +330,11 @@ __device__ __forceinline__ unsigned long long global_ns() {
 
 // One bounded-wait check, every 256 polls of a spin: false = give up (the
 // launch is aborted, or this wait exceeded spin_ns and aborts it).
-__device__ __forceinline__ bool keep_waiting(unsigned n, unsigned long long& t0, int lane, const SweepFail& F) {
-    if ((n & 255u) != 255u) return true;
+// (The slow paths of the waits are out of line: the chain warp's per-group
+// control code stays small and next to its step block in the instruction
+// cache; ncu shows stall_no_instruction leading in the inlined wait code.)
+// (everything by value: a reference would put the caller's variable on the stack)
+__device__ __noinline__ unsigned long long keep_waiting_check(unsigned long long t0, int lane, SweepFail F) {
     int ab = 0;
     if (lane == 0) {
         const unsigned long long now = global_ns();
@@ -343,7 +346,13 @@ __device__ __forceinline__ bool keep_waiting(unsigned n, unsigned long long& t0,
             ab = 1;
         }
     }
-    return !__shfl_sync(kFull, ab, 0);
+    t0 = __shfl_sync(kFull, t0, 0);
+    return __shfl_sync(kFull, ab, 0) ? ~0ull : t0;  // ~0: give up
+}
+__device__ __forceinline__ bool keep_waiting(unsigned n, unsigned long long& t0, int lane, const SweepFail& F) {
+    if ((n & 255u) != 255u) return true;
+    t0 = keep_waiting_check(t0, lane, F);
+    return t0 != ~0ull;
 }
 
 template <int K, int CK>
@@ -360,19 +369,40 @@ __device__ __forceinline__ bool chunk_complete(float4 q, int u0, int Umax, int l
 // Poll chunk u0 / CK of the band above until every word of it is written;
 // leaves it in the chunk buffer.  `v` holds a load issued earlier and is
 // re-polled only while incomplete.
+struct ChunkPoll {
+    float4 v;
+    bool ok;
+};
 template <int K, int CK>
-__device__ __forceinline__ bool acquire_chunk(float4 v, const float* up_stream, int u0, int Umax, int lane,
-                                              int chunk, const SweepFail& F) {
+__device__ __noinline__ ChunkPoll acquire_chunk_spin(const float* up_stream, int u0, int Umax, int lane, SweepFail F) {
     using G = Geom<K, CK>;
     const int nvalid = min(CK, Umax - u0) * K * 2;
     const bool mine = lane < G::CH4 && 4 * lane < nvalid;
     unsigned long long t0 = 0;
-    for (unsigned n = 0; !__all_sync(kFull, chunk_complete<K, CK>(v, u0, Umax, lane)); ++n) {
+    ChunkPoll r;
+    r.v = make_float4(0.f, 0.f, 0.f, 0.f);
+    r.ok = true;
+    for (unsigned n = 0;; ++n) {
         if (CK > 4) __nanosleep(32);  // (4-column chunks: latency-bound launches, the load's round trip is the poll interval)
-        if (mine) v = ld_relaxed_v4(up_stream + size_t(u0) * K * 2 + 4 * lane);
-        if (!keep_waiting(n, t0, lane, F)) return false;
+        if (mine) r.v = ld_relaxed_v4(up_stream + size_t(u0) * K * 2 + 4 * lane);
+        if (__all_sync(kFull, chunk_complete<K, CK>(r.v, u0, Umax, lane))) return r;
+        if (!keep_waiting(n, t0, lane, F)) {
+            r.ok = false;
+            return r;
+        }
     }
-    if (mine) sts4(chunk + 4 * lane, v);
+}
+template <int K, int CK>
+__device__ __forceinline__ bool acquire_chunk(float4 v, const float* up_stream, int u0, int Umax, int lane,
+                                              int chunk, const SweepFail& F) {
+    using G = Geom<K, CK>;
+    if (!__all_sync(kFull, chunk_complete<K, CK>(v, u0, Umax, lane))) {
+        const ChunkPoll r = acquire_chunk_spin<K, CK>(up_stream, u0, Umax, lane, F);
+        if (!r.ok) return false;
+        v = r.v;
+    }
+    const int nvalid = min(CK, Umax - u0) * K * 2;
+    if (lane < G::CH4 && 4 * lane < nvalid) sts4(chunk + 4 * lane, v);
     return true;
 }
 
@@ -380,14 +410,17 @@ __device__ __forceinline__ bool acquire_chunk(float4 v, const float* up_stream, 
 // counter); returns the value seen, or -1 when aborted.  Called by a converged
 // warp: every lane reads the same word in the same instruction (a broadcast),
 // so the value and the branches on it are warp-uniform.
-__device__ __forceinline__ int wait_progress(unsigned saddr, int need, int lane, const SweepFail& F) {
+__device__ __noinline__ int wait_progress_spin(unsigned saddr, int need, int lane, SweepFail F) {
     unsigned long long t0 = 0;
-    int v = ld_volatile_cta(saddr);
-    for (unsigned n = 0; v < need; ++n) {
+    for (unsigned n = 0;; ++n) {
         if (!keep_waiting(n, t0, lane, F)) return -1;
-        v = ld_volatile_cta(saddr);
+        const int v = ld_volatile_cta(saddr);
+        if (v >= need) return v;
     }
-    return v;
+}
+__device__ __forceinline__ int wait_progress(unsigned saddr, int need, int lane, const SweepFail& F) {
+    const int v = ld_volatile_cta(saddr);
+    return v >= need ? v : wait_progress_spin(saddr, need, lane, F);
 }
 
 // ---- chain warps -------------------------------------------------------------
