@@ -798,31 +798,36 @@ __device__ __forceinline__ bool run_chain(const SweepJob& J, int q, int ch, int 
                 __syncwarp();
             }
             TR(3);
+            // (block order: the cold variants first; the interior block and, last,
+            // the first band's -- the band that paces every other -- fall through
+            // to the group's tail)
             const bool xin = t4 >= bg.fast_lo && t4 + S <= bg.fast_hi;
-            if (xin && !bg.yband) {
-                const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
+            if (!xin) {
+                if (t4 < bg.fast_lo && t4 + S <= bg.fast_hi) {  // band start: left border only
+                    const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
+                    if (bg.yband) {
 #pragma unroll
-                for (int s = 0; s < S; ++s) chain_step<K, false, CK>(st, cx, t4 + s, &ga, s);
-            } else if (xin && bg.ytop) {  // the first band of a taller image: U clamps only
-                const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
+                        for (int s = 0; s < S; ++s) chain_step<K, false, CK, true, true, true>(st, cx, t4 + s, &ga, s);
+                    } else {
 #pragma unroll
-                for (int s = 0; s < S; ++s) chain_step<K, false, CK, true, false>(st, cx, t4 + s, &ga, s);
-            } else if (xin) {
+                        for (int s = 0; s < S; ++s) chain_step<K, false, CK, false, false, true>(st, cx, t4 + s, &ga, s);
+                    }
+                } else {
+#pragma unroll 1
+                    for (int s = 0; s < S; ++s) chain_step<K, true, CK>(st, cx, t4 + s);
+                }
+            } else if (bg.yband && !bg.ytop) {
                 const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
 #pragma unroll
                 for (int s = 0; s < S; ++s) chain_step<K, false, CK, true, true>(st, cx, t4 + s, &ga, s);
-            } else if (t4 < bg.fast_lo && t4 + S <= bg.fast_hi) {  // band start: left border only
+            } else if (!bg.yband) {
                 const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
-                if (bg.yband) {
 #pragma unroll
-                    for (int s = 0; s < S; ++s) chain_step<K, false, CK, true, true, true>(st, cx, t4 + s, &ga, s);
-                } else {
+                for (int s = 0; s < S; ++s) chain_step<K, false, CK>(st, cx, t4 + s, &ga, s);
+            } else {  // the first band of a taller image: U clamps only
+                const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
 #pragma unroll
-                    for (int s = 0; s < S; ++s) chain_step<K, false, CK, false, false, true>(st, cx, t4 + s, &ga, s);
-                }
-            } else {
-#pragma unroll 1
-                for (int s = 0; s < S; ++s) chain_step<K, true, CK>(st, cx, t4 + s);
+                for (int s = 0; s < S; ++s) chain_step<K, false, CK, true, false>(st, cx, t4 + s, &ga, s);
             }
         }
         TR(4);
