@@ -887,15 +887,15 @@ __device__ __forceinline__ bool run_helper(const SweepJob& J, int q, int ch, int
         const bool xin = t4 >= bg.fast_lo && t4 + S <= bg.fast_hi;
         if (xin && !bg.yband) {
             const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
-#pragma unroll
+#pragma unroll 1
             for (int s = 0; s < S; ++s) flush_step<K, false, CK>(cx, t4 + s, &ga, s);
         } else if (xin) {
             const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
-#pragma unroll
+#pragma unroll 1
             for (int s = 0; s < S; ++s) flush_step<K, false, CK, true>(cx, t4 + s, &ga, s);
         } else if (t4 < bg.fast_lo && t4 + S <= bg.fast_hi) {  // band start: segments left of column 0 are skipped
             const GroupAddr<K> ga = group_addr<K, CK>(cx, t4);
-#pragma unroll
+#pragma unroll 1
             for (int s = 0; s < S; ++s) flush_step<K, false, CK, true, true>(cx, t4 + s, &ga, s);
         } else {
 #pragma unroll 1
